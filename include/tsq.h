@@ -1,0 +1,153 @@
+/*
+ * include/tsq.h -- C ABI of the B200 three-way partition sort
+ * (libtsq_b200.so, built from paper_1505_00558_b200/csrc/).
+ *
+ * Drop-in boundary.  The reference (tsqsort 0.1.0, pure Python) has no FFI;
+ * its sort path is the Python API below, and each entry point here is what a
+ * native binding of that API calls (the ctypes stub a maintainer would add to
+ * the reference is shown in INTEGRATION.md):
+ *
+ *   tsq_sort              <- Sorter.sort_with_stats / tsqsort.sort
+ *                            (/root/reference/pkg/src/tsqsort/core.py:1586-1614,
+ *                             core.py:1757-1770); in place, returns counters
+ *   tsq_workspace_*       <- TempStore.ensure / release and
+ *                            Sorter.free_temp_storage (core.py:81-104,
+ *                            core.py:1616-1620): a retained, high-water
+ *                            device workspace owned by one sorter
+ *   tsq_partition_segment <- the per-stage contract entry points
+ *                            init_stage .. copy_back (core.py:1789-1870):
+ *                            one three-way partition of one segment around a
+ *                            given pivot, returning the stage bounds
+ *   tsq_select_pivot      <- select_pivot (pivot.py:205-248): the device
+ *                            pivot-sampling kernel on one segment
+ *
+ * Conventions: plain pointers and sizes; `keys`/`payload` are DEVICE
+ * pointers owned by the caller and sorted in place; work is enqueued on the
+ * given cudaStream_t (passed as void*, NULL = legacy default stream); calls
+ * that return statistics synchronise that stream.  One call in flight per
+ * workspace (the reference's non-reentrancy rule, core.py:1589-1590).
+ * Keys compare with the native order of their type (IEEE order for floats,
+ * -0.0 placed before +0.0, NaNs after +inf / before -inf by sign bit).
+ */
+#ifndef TSQ_H
+#define TSQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSQ_ABI_VERSION 1
+
+typedef enum {
+  TSQ_OK = 0,
+  TSQ_ERR_ALLOC = 1,              /* -> TempAllocationError (core.py:46-47) */
+  TSQ_ERR_UNSUPPORTED_DTYPE = 2,  /* -> TypeError */
+  TSQ_ERR_CUDA = 3,               /* -> RuntimeError */
+  TSQ_ERR_DEPTH_EXCEEDED = 4,     /* depth guard tripped (no O(n^2) fallback) */
+  TSQ_ERR_INVALID = 5,            /* -> ValueError (bad sizes / pointers) */
+  TSQ_ERR_BUSY = 6,               /* -> RuntimeError("not reentrant") */
+  TSQ_ERR_CAPACITY = 7            /* internal queue overflow */
+} tsq_status;
+
+typedef enum {
+  TSQ_NONE = 0,
+  TSQ_I32 = 1,
+  TSQ_U32 = 2,
+  TSQ_I64 = 3,
+  TSQ_U64 = 4,
+  TSQ_F32 = 5,
+  TSQ_F64 = 6
+} tsq_dtype;
+
+/* GPU knobs (kept apart from SortConfig, whose validation caps
+ * insertion_threshold below 70, config.py:31-38). 0 = default. */
+typedef struct {
+  double dran;             /* MitigationRng.dran in [0.5,1.5) (pivot.py:45-49); 0 -> 1.0 */
+  int32_t mitigation;      /* jitter sample positions by dran (config.py:24) */
+  int32_t fast_paths;      /* sorted/reversed verify-and-bypass (core.py:1678-1698); default 1 */
+  int32_t max_depth;       /* depth guard; default 96 */
+  int32_t host_levels;     /* 1 = drive levels from the host (debug/per-level stats) */
+  int32_t small_threshold; /* segments <= this go on chip (1..4096); default 4096 */
+  int32_t reserved0;
+  int64_t reserved[3];
+} tsq_params;
+
+/* Counters of one call (the SortStats analogue, stats.py:33-70). */
+typedef struct {
+  uint64_t n;
+  uint64_t stages;             /* segments partitioned or verified on device */
+  uint64_t levels;             /* device partition levels (HBM passes) */
+  uint64_t max_depth;          /* deepest recursion level reached */
+  uint64_t small_segments;     /* segments finished by the on-chip sort */
+  uint64_t eq_runs;            /* ==p runs retired */
+  uint64_t eq_elements;        /* keys retired inside ==p runs */
+  uint64_t sorted_bypass;      /* stages verified sorted (no migration) */
+  uint64_t reversed_bypass;    /* stages verified reversed (mirrored) */
+  uint64_t verify_fallbacks;   /* verification failed -> partitioned */
+  uint64_t partitioned_elements;
+  uint64_t bytes_partition;    /* algorithmic HBM bytes of the level kernels */
+  uint64_t bytes_small;        /* ... of the on-chip sort */
+  uint64_t bytes_retire;       /* ... of run retirement (fills / copies) */
+  uint64_t temp_high_water;    /* workspace elements reserved */
+  uint64_t error_flags;
+  uint64_t writes_caller;      /* element writes into the caller's array */
+  uint64_t writes_workspace;   /* element writes into the workspace */
+  float ms_levels;             /* device time of the level loop (events) */
+  float ms_total;              /* device time of the whole sort (events) */
+} tsq_stats;
+
+typedef struct tsq_workspace tsq_workspace;
+
+const char *tsq_status_str(tsq_status s);
+int tsq_abi_version(void);
+
+/* Workspace lifecycle (TempStore, core.py:81-104). */
+tsq_status tsq_workspace_create(tsq_workspace **out, int device);
+void tsq_workspace_destroy(tsq_workspace *ws);
+/* bytes of device memory a sort of n elements needs */
+size_t tsq_workspace_bytes(size_t n, tsq_dtype key_t, tsq_dtype payload_t);
+/* reserve for n elements; keeps the high water (no shrink) */
+tsq_status tsq_workspace_reserve(tsq_workspace *ws, size_t n, tsq_dtype key_t,
+                                 tsq_dtype payload_t);
+/* release device memory; the next sort reallocates (free_temp_storage) */
+tsq_status tsq_workspace_free(tsq_workspace *ws);
+/* elements the workspace currently holds capacity for; allocation count */
+size_t tsq_workspace_capacity(const tsq_workspace *ws);
+uint64_t tsq_workspace_alloc_count(const tsq_workspace *ws);
+
+/* Sort keys[0..n) ascending in place; payload (nullable, TSQ_U32) moves with
+ * its key (records compared by key only).  stats may be NULL (no sync). */
+tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t,
+                    tsq_dtype payload_t, const tsq_params *params,
+                    tsq_workspace *ws, void *stream, tsq_stats *stats);
+
+/* Per-level trace of the last host_levels sort (the stage_hook / trace
+ * analogue, core.py:1705-1710): device ms, live segments and tiles per
+ * level.  Returns the number of levels (may exceed cap). */
+int tsq_level_trace(const tsq_workspace *ws, float *ms, uint32_t *segments,
+                    uint32_t *tiles, int cap);
+
+/* One stage: three-way partition of keys[0..n) around `pivot` (raw bits of a
+ * key of key_t), out of place into out_keys (and out_payload), < from the
+ * front, > from the back, == in the middle.  Writes new_l = n_lt - 1 and
+ * new_r = n - n_gt (stage law, reference tests/conftest.py:37-45). Syncs. */
+tsq_status tsq_partition_segment(const void *keys, const void *payload,
+                                 void *out_keys, void *out_payload, size_t n,
+                                 tsq_dtype key_t, tsq_dtype payload_t,
+                                 uint64_t pivot, tsq_workspace *ws,
+                                 void *stream, int64_t *new_l, int64_t *new_r);
+
+/* Device pivot sampling of keys[0..n): writes the chosen pivot (raw bits)
+ * and the sample order flag (+1 nondecreasing, -1 nonincreasing, 0).  Syncs. */
+tsq_status tsq_select_pivot(const void *keys, size_t n, tsq_dtype key_t,
+                            double dran, int32_t mitigation,
+                            tsq_workspace *ws, void *stream,
+                            uint64_t *pivot, int32_t *order_flag);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

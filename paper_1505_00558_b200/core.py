@@ -1,0 +1,423 @@
+"""Reference-facing sort API over the B200 kernels.
+
+Mirrors tsqsort's public sort path (/root/reference/pkg/src/tsqsort/core.py):
+
+  * ``Sorter(config=None, seed=None)``            core.py:1572-1579
+  * ``Sorter.sort`` / ``sort_with_stats``          core.py:1583-1614
+  * ``Sorter.free_temp_storage``                   core.py:1616-1620
+  * module ``sort`` / ``sort_with_stats`` / ``free_temp_storage`` and the
+    retained ``default_sorter``                    core.py:1754-1774
+  * ``TempAllocationError``                        core.py:46-47
+
+with the same argument meanings and error behaviour: ``ar`` is sorted in
+place, a fresh ``SortStats`` is returned, the workspace is retained across
+calls until ``free_temp_storage``, an instance is not reentrant, allocation
+happens before any mutation.  All sorting runs in libtsq_b200.so on the GPU;
+there is no CPU fallback -- unsupported inputs raise.
+
+Accepted containers for ``ar``:
+  * a 1-D CUDA tensor (int32/uint32/int64/uint64/float32/float64): in place
+  * a CPU tensor or numpy array of those dtypes: staged through the GPU
+  * a Python list of ints or floats: converted, sorted, written back
+  * ``Records(keys, payload)`` (or a ``(keys, payload)`` tuple of tensors /
+    arrays) with a uint32 payload: keys sorted, payload moved with its key
+  * a list of ``(key, payload)`` tuples with ``cmp=key_cmp`` -- the
+    reference's key-only comparator pattern (tests/test_core.py:93-103)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .config import DEFAULT_CONFIG, DEFAULT_GPU_CONFIG, GpuConfig, SortConfig
+from .pivot import MitigationRng
+from .stats import SortStats
+
+__all__ = ["TempAllocationError", "DepthExceededError", "Records", "key_cmp",
+           "DeviceTempStore", "Sorter", "sort", "sort_with_stats", "free_temp_storage",
+           "default_sorter"]
+
+
+class TempAllocationError(MemoryError):
+    """The device workspace could not be allocated (array left untouched)."""
+
+
+class DepthExceededError(RuntimeError):
+    """The device recursion exceeded GpuConfig.max_depth."""
+
+
+def key_cmp(x, y) -> int:
+    """Key-only comparator for (key, payload) records: compares x[0], y[0]."""
+    a, b = x[0], y[0]
+    return -1 if a < b else (1 if a > b else 0)
+
+
+@dataclass
+class Records:
+    """Keys plus a uint32 payload that moves with its key."""
+
+    keys: object
+    payload: object
+
+
+_TORCH_DT = None
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_codes():
+    global _TORCH_DT
+    if _TORCH_DT is None:
+        torch = _torch()
+        _TORCH_DT = {
+            torch.int32: N.TSQ_I32, torch.uint32: N.TSQ_U32, torch.int64: N.TSQ_I64,
+            torch.uint64: N.TSQ_U64, torch.float32: N.TSQ_F32, torch.float64: N.TSQ_F64,
+        }
+    return _TORCH_DT
+
+
+def _raise_status(st: int, what: str):
+    if st == N.TSQ_OK:
+        return
+    if st == N.TSQ_ERR_ALLOC:
+        raise TempAllocationError(f"{what}: cannot allocate the device workspace")
+    if st == N.TSQ_ERR_UNSUPPORTED_DTYPE:
+        raise TypeError(f"{what}: unsupported dtype")
+    if st == N.TSQ_ERR_INVALID:
+        raise ValueError(f"{what}: invalid argument")
+    if st == N.TSQ_ERR_BUSY:
+        raise RuntimeError("sorter instance is not reentrant")
+    if st == N.TSQ_ERR_DEPTH_EXCEEDED:
+        raise DepthExceededError(f"{what}: recursion depth guard exceeded")
+    raise N.TsqError(st, what)
+
+
+class DeviceTempStore:
+    """Retained device workspace (TempStore, core.py:81-104).
+
+    ``capacity`` is the element count of the largest sort served since the
+    last release; ``alloc_count`` counts device allocations.
+    """
+
+    def __init__(self, device: int | None = None):
+        self.device = device
+        self._ws = None
+
+    def workspace(self) -> N.Workspace:
+        if self._ws is None:
+            torch = _torch()
+            if not torch.cuda.is_available():
+                raise RuntimeError("no CUDA device: the B200 sort has no CPU fallback")
+            dev = torch.cuda.current_device() if self.device is None else self.device
+            self.device = dev
+            self._ws = N.Workspace(dev)
+        return self._ws
+
+    @property
+    def capacity(self) -> int:
+        return self._ws.capacity if self._ws is not None else 0
+
+    @property
+    def alloc_count(self) -> int:
+        return self._ws.alloc_count if self._ws is not None else 0
+
+    def ensure(self, n: int, key_dt: int = N.TSQ_I32, pay_dt: int = N.TSQ_NONE) -> None:
+        _raise_status(self.workspace().reserve(n, key_dt, pay_dt), "workspace reserve")
+
+    def release(self) -> None:
+        if self._ws is not None:
+            _raise_status(self._ws.free(), "workspace free")
+
+
+class _Job:
+    """One sort call's device tensors and how to write results back."""
+
+    __slots__ = ("keys", "payload", "n", "key_dt", "pay_dt", "finish", "h2d_bytes",
+                 "d2h_bytes")
+
+    def __init__(self):
+        self.keys = None
+        self.payload = None
+        self.n = 0
+        self.key_dt = N.TSQ_NONE
+        self.pay_dt = N.TSQ_NONE
+        self.finish = None
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+
+def _list_to_numpy(values) -> np.ndarray:
+    if all(isinstance(v, (bool, int, np.integer)) for v in values):
+        try:
+            return np.asarray(values, dtype=np.int64)
+        except OverflowError:
+            try:
+                return np.asarray(values, dtype=np.uint64)
+            except OverflowError:
+                raise TypeError("integers beyond 64 bits are not supported on the GPU path")
+    if all(isinstance(v, (float, np.floating)) for v in values):
+        return np.asarray(values, dtype=np.float64)
+    raise TypeError("lists must hold only ints or only floats on the GPU path "
+                    "(custom element types need a comparator the device cannot run)")
+
+
+class Sorter:
+    """A sorter instance: config, mitigation generator, retained workspace.
+
+    Not reentrant (core.py:1589-1590); distinct instances are independent.
+    """
+
+    def __init__(self, config: SortConfig | None = None, seed: int | None = None,
+                 gpu: GpuConfig | None = None, device: int | None = None):
+        self.config = config if config is not None else DEFAULT_CONFIG
+        self.gpu = gpu if gpu is not None else DEFAULT_GPU_CONFIG
+        self.rng = MitigationRng(seed)
+        self.temp = DeviceTempStore(device)
+        self.stage_hook = None
+        self.trace = None
+        self.last_level_trace = None
+        self._active = False
+        self._lock = threading.Lock()
+        self._staging = {}
+
+    # -- public API --
+
+    def sort(self, ar, cmp=None, element_size: int | None = None) -> None:
+        self.sort_with_stats(ar, cmp, element_size)
+
+    def sort_with_stats(self, ar, cmp=None, element_size: int | None = None) -> SortStats:
+        """Sort ``ar`` in place on the GPU; returns the run's counters."""
+        with self._lock:
+            if self._active:
+                raise RuntimeError("sorter instance is not reentrant")
+            self._active = True
+        try:
+            return self._sort(ar, cmp, element_size)
+        finally:
+            self._active = False
+
+    def free_temp_storage(self) -> None:
+        """Release the retained workspace; the next sort reallocates."""
+        if self._active:
+            raise RuntimeError("cannot free temp storage during a sort")
+        self.temp.release()
+        self._staging.clear()
+
+    # -- internals --
+
+    def _device(self) -> int:
+        self.temp.workspace()
+        return self.temp.device
+
+    def _stage(self, host, slot: str):
+        """Device copy of a host tensor through a retained staging buffer."""
+        torch = _torch()
+        dev = self._device()
+        buf = self._staging.get(slot)
+        if buf is None or buf.dtype != host.dtype or buf.numel() < host.numel():
+            try:
+                buf = torch.empty(host.numel(), dtype=host.dtype, device=f"cuda:{dev}")
+            except torch.OutOfMemoryError as exc:
+                raise TempAllocationError("cannot allocate the device staging buffer") from exc
+            self._staging[slot] = buf
+        d = buf[:host.numel()]
+        d.copy_(host, non_blocking=True)
+        return d
+
+    def _prepare(self, ar, cmp) -> _Job:
+        torch = _torch()
+        codes = _dtype_codes()
+        job = _Job()
+        if cmp is not None and cmp is not key_cmp:
+            raise TypeError("custom comparators cannot run on the GPU path; pass cmp=None "
+                            "(native order) or cmp=key_cmp for (key, payload) records")
+        # records given as separate arrays
+        if isinstance(ar, Records) or (isinstance(ar, tuple) and len(ar) == 2 and
+                                       all(isinstance(x, (np.ndarray, torch.Tensor)) for x in ar)):
+            keys, pay = (ar.keys, ar.payload) if isinstance(ar, Records) else ar
+            kt = keys if isinstance(keys, torch.Tensor) else torch.from_numpy(keys)
+            pt = pay if isinstance(pay, torch.Tensor) else torch.from_numpy(pay)
+            if pt.dtype != torch.uint32 or pt.shape != kt.shape or kt.dim() != 1:
+                raise TypeError("records need 1-D keys and a uint32 payload of the same length")
+            self._bind(job, kt, pt, codes)
+            return job
+        if isinstance(ar, np.ndarray):
+            ar_t = torch.from_numpy(ar) if ar.flags.c_contiguous else None
+            if ar_t is None:
+                raise ValueError("numpy input must be C-contiguous")
+            self._bind(job, ar_t, None, codes)
+            return job
+        if isinstance(ar, torch.Tensor):
+            self._bind(job, ar, None, codes)
+            return job
+        # generic Python sequence
+        values = list(ar)
+        n = len(values)
+        job.n = n
+        if n <= 1:
+            return job
+        if cmp is key_cmp:
+            keys = _list_to_numpy([v[0] for v in values])
+            pay = np.arange(n, dtype=np.uint32)
+            kt = torch.from_numpy(keys)
+            pt = torch.from_numpy(pay)
+            self._bind(job, kt, pt, codes)
+            inner = job.finish
+
+            def finish_records():
+                inner()
+                perm = pay
+                ar[:] = [values[i] for i in perm.tolist()]
+
+            job.finish = finish_records
+            return job
+        arr = _list_to_numpy(values)
+        kt = torch.from_numpy(arr)
+        self._bind(job, kt, None, codes)
+        inner = job.finish
+
+        def finish_list():
+            inner()
+            ar[:] = arr.tolist()
+
+        job.finish = finish_list
+        return job
+
+    def _bind(self, job: _Job, keys, payload, codes):
+        torch = _torch()
+        if keys.dim() != 1:
+            raise ValueError("keys must be one-dimensional")
+        if keys.dtype not in codes:
+            raise TypeError(f"unsupported key dtype {keys.dtype}")
+        job.n = keys.numel()
+        job.key_dt = codes[keys.dtype]
+        job.pay_dt = N.TSQ_U32 if payload is not None else N.TSQ_NONE
+        if job.n <= 1:
+            job.finish = lambda: None
+            return
+        outs = []
+        devs = []
+        for slot, t in (("keys", keys), ("payload", payload)):
+            if t is None:
+                devs.append(None)
+                continue
+            if t.is_cuda:
+                if t.is_contiguous():
+                    devs.append(t)
+                else:
+                    d = t.contiguous()
+                    devs.append(d)
+                    outs.append((t, d))
+            else:
+                host = t if t.is_contiguous() else t.contiguous()
+                d = self._stage(host, slot)
+                job.h2d_bytes += host.numel() * host.element_size()
+                devs.append(d)
+                outs.append((t, d))
+        job.keys, job.payload = devs
+
+        def finish():
+            if not outs:
+                return
+            for dst, src in outs:
+                dst.copy_(src, non_blocking=not dst.is_cuda)
+                if not dst.is_cuda:
+                    job.d2h_bytes += dst.numel() * dst.element_size()
+            torch.cuda.current_stream(src.device).synchronize()
+
+        job.finish = finish
+
+    def _sort(self, ar, cmp, element_size) -> SortStats:
+        if element_size is not None and element_size >= self.config.late_swap_byte_threshold:
+            raise NotImplementedError(
+                "late swapping (element_size >= late_swap_byte_threshold, bigelem.py) is "
+                "outside the GPU sort path")
+        job = self._prepare(ar, cmp)
+        stats = SortStats()
+        if job.n <= 1:
+            return stats
+        torch = _torch()
+        # allocation precedes any mutation (core.py:1599): the array stays
+        # untouched if this raises
+        self.temp.ensure(job.n, job.key_dt, job.pay_dt)
+        self.rng.next()
+        p = N.TsqParams()
+        p.dran = self.rng.dran
+        p.mitigation = 1 if self.config.mitigation_enabled else 0
+        p.fast_paths = 1 if self.gpu.fast_paths else 0
+        p.max_depth = self.gpu.max_depth
+        p.small_threshold = self.gpu.small_threshold
+        p.host_levels = 1 if (self.gpu.host_levels or self.stage_hook is not None) else 0
+        ts = N.TsqStats()
+        dev = job.keys.device
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ws = self.temp.workspace()
+        st = N.lib().tsq_sort(
+            ctypes.c_void_p(job.keys.data_ptr()),
+            ctypes.c_void_p(job.payload.data_ptr()) if job.payload is not None else None,
+            job.n, job.key_dt, job.pay_dt, ctypes.byref(p), ws.handle,
+            ctypes.c_void_p(stream), ctypes.byref(ts))
+        _raise_status(st, "tsq_sort")
+        if p.host_levels:
+            self.last_level_trace = ws.level_trace()
+            if self.stage_hook is not None:
+                for i, lv in enumerate(self.last_level_trace):
+                    self.stage_hook(i, lv)
+        job.finish()
+        return _to_stats(ts, job)
+
+
+def _to_stats(ts: N.TsqStats, job: _Job) -> SortStats:
+    s = SortStats()
+    s.comparisons = int(ts.partitioned_elements)
+    s.array_writes = int(ts.writes_caller)
+    s.scratch_writes = int(ts.writes_workspace)
+    s.element_writes = s.array_writes + s.scratch_writes
+    s.temp_high_water = int(ts.temp_high_water)
+    s.max_depth = int(ts.max_depth)
+    s.stages = int(ts.stages)
+    s.state_activations = {"partition": int(ts.stages - ts.sorted_bypass - ts.reversed_bypass),
+                           "eq_run": int(ts.eq_runs), "small": int(ts.small_segments)}
+    s.handler_activations = {"sorted": int(ts.sorted_bypass),
+                             "reversed": int(ts.reversed_bypass),
+                             "fallbacks": int(ts.verify_fallbacks)}
+    g = ts.as_dict()
+    g["h2d_bytes"] = job.h2d_bytes
+    g["d2h_bytes"] = job.d2h_bytes
+    s.gpu = g
+    return s
+
+
+# ---------------------------------------------------------------------------
+# Module-level convenience API around a default retained instance
+# (core.py:1754-1774).
+
+default_sorter = Sorter()
+
+
+def sort(ar, cmp=None, config: SortConfig | None = None,
+         element_size: int | None = None) -> SortStats:
+    """Sort in place with the module's default sorter instance."""
+    global default_sorter
+    if config is not None and config != default_sorter.config:
+        fresh = Sorter(config, seed=default_sorter.rng.zgen, gpu=default_sorter.gpu)
+        fresh.temp = default_sorter.temp  # keep the retained workspace
+        default_sorter = fresh
+    return default_sorter.sort_with_stats(ar, cmp, element_size)
+
+
+def sort_with_stats(ar, cmp=None, config: SortConfig | None = None,
+                    element_size: int | None = None) -> SortStats:
+    return sort(ar, cmp, config, element_size)
+
+
+def free_temp_storage() -> None:
+    default_sorter.free_temp_storage()

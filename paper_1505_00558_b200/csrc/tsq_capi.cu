@@ -1,0 +1,673 @@
+// tsq_capi.cu -- host side of libtsq_b200.so: workspace (the retained
+// TempStore analogue, core.py:81-104), the CUDA-graph driver of the device
+// recursion (Sorter._range, core.py:1643-1728, with no per-level host round
+// trip: a conditional WHILE node re-launches the level kernel until the
+// device queue is empty), and the extern "C" entry points of include/tsq.h.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "tsq_kernels.cuh"
+
+using namespace tsq;
+
+namespace {
+
+struct KernelSet {
+  const void *init, *level, *small, *retire, *selp;
+  int key_bytes, tile;
+  size_t small_smem;
+};
+
+template <int DT, bool PAY>
+KernelSet make_set() {
+  typedef Codec<DT> C;
+  KernelSet s;
+  s.init = reinterpret_cast<const void *>(&init_kernel<C, PAY>);
+  s.level = reinterpret_cast<const void *>(&level_kernel<C, PAY>);
+  s.small = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY>);
+  s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
+  s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
+  s.key_bytes = (int)sizeof(typename C::U);
+  s.tile = Geo<C, PAY>::TILE;
+  s.small_smem = (size_t)kSmallT * (sizeof(typename C::U) + (PAY ? 6 : 0));
+  return s;
+}
+
+bool get_set(int dt, bool pay, KernelSet *out) {
+#define TSQ_CASE(D)                                          \
+  case D:                                                    \
+    *out = pay ? make_set<D, true>() : make_set<D, false>(); \
+    return true;
+  switch (dt) {
+    TSQ_CASE(TSQ_I32)
+    TSQ_CASE(TSQ_U32)
+    TSQ_CASE(TSQ_F32)
+    TSQ_CASE(TSQ_I64)
+    TSQ_CASE(TSQ_U64)
+    TSQ_CASE(TSQ_F64)
+    default:
+      return false;
+  }
+#undef TSQ_CASE
+}
+
+int key_bytes_of(int dt) {
+  switch (dt) {
+    case TSQ_I32: case TSQ_U32: case TSQ_F32: return 4;
+    case TSQ_I64: case TSQ_U64: case TSQ_F64: return 8;
+    default: return 0;
+  }
+}
+
+// host copies of the order-preserving codecs (for given pivots)
+u64 host_enc(int dt, u64 x) {
+  switch (dt) {
+    case TSQ_I32: return (x ^ 0x80000000ull) & 0xffffffffull;
+    case TSQ_U32: return x & 0xffffffffull;
+    case TSQ_F32: { uint32_t v = (uint32_t)x; return (u64)(v ^ ((0u - (v >> 31)) | 0x80000000u)); }
+    case TSQ_I64: return x ^ 0x8000000000000000ull;
+    case TSQ_U64: return x;
+    case TSQ_F64: return x ^ ((0ull - (x >> 63)) | 0x8000000000000000ull);
+    default: return x;
+  }
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t keys_alt, pay_alt, side_pay, segs[2], tilemap[2], lookback[2], smalls, runs, chunkmap;
+  size_t total;
+  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap;
+};
+
+Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallT) {
+  Layout L;
+  memset(&L, 0, sizeof(L));
+  const int kb = key_bytes_of(kt);
+  const size_t tile = kb == 4 ? 4096 : 2048;
+  const bool pay = pt == TSQ_U32;
+  L.seg_cap = (uint32_t)(n / (size_t)small_t + 2);
+  L.tile_cap = (uint32_t)(n / tile + 2ull * L.seg_cap + 2);
+  L.run_cap = 8u * L.seg_cap + 64u;
+  L.small_cap = 2u * L.run_cap;
+  L.chunk_cap = (uint32_t)(n / kRunChunk + L.run_cap + 2);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  L.keys_alt = take(n * kb + 64);
+  L.pay_alt = take(pay ? n * 4 + 64 : 0);
+  L.side_pay = take(pay ? n * 4 + 64 : 0);
+  for (int b = 0; b < 2; ++b) L.segs[b] = take((size_t)L.seg_cap * sizeof(Seg));
+  for (int b = 0; b < 2; ++b) L.tilemap[b] = take((size_t)L.tile_cap * 4);
+  for (int b = 0; b < 2; ++b) L.lookback[b] = take((size_t)L.tile_cap * 8);
+  L.smalls = take((size_t)L.small_cap * sizeof(SmallSeg));
+  L.runs = take((size_t)L.run_cap * sizeof(Run));
+  L.chunkmap = take((size_t)L.chunk_cap * 4);
+  L.total = off;
+  return L;
+}
+
+struct GraphEntry {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t init_node = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaKernelNodeParams init_params;
+};
+
+}  // namespace
+
+struct tsq_workspace {
+  int device = 0;
+  int num_sms = 148;
+  void *block = nullptr;
+  size_t block_bytes = 0;
+  size_t cap_elems = 0;
+  uint64_t alloc_count = 0;
+  Params *d_params = nullptr;
+  Ctl *d_ctl = nullptr;
+  Ctl *h_ctl = nullptr;
+  cudaEvent_t done = nullptr;
+  bool active = false;
+  std::mutex mu;
+  std::map<int, GraphEntry> graphs;
+  std::vector<float> level_ms;      // host_levels mode trace
+  std::vector<uint32_t> level_segs, level_tiles;
+};
+
+#define TSQ_CUDA(call)                                     \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) {                               \
+      fprintf(stderr, "tsq: %s failed: %s (%s:%d)\n", #call, \
+              cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return TSQ_ERR_CUDA;                                 \
+    }                                                      \
+  } while (0)
+
+namespace {
+
+int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  return occ * ws->num_sms;
+}
+
+tsq_status prepare_small_smem(const KernelSet &ks) {
+  if (ks.small_smem > 48 * 1024)
+    TSQ_CUDA(cudaFuncSetAttribute(ks.small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ks.small_smem));
+  return TSQ_OK;
+}
+
+void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void *payload,
+                 size_t n) {
+  memset(p, 0, sizeof(*p));
+  char *base = reinterpret_cast<char *>(ws->block);
+  p->keys[0] = keys;
+  p->keys[1] = base + L.keys_alt;
+  p->pay[0] = reinterpret_cast<uint32_t *>(payload);
+  p->pay[1] = payload ? reinterpret_cast<uint32_t *>(base + L.pay_alt) : nullptr;
+  p->side_pay = payload ? reinterpret_cast<uint32_t *>(base + L.side_pay) : nullptr;
+  p->n = (long long)n;
+  p->raw[0] = 1;
+  p->raw[1] = 0;
+  const bool a0 = ((uintptr_t)keys % 16 == 0) && ((uintptr_t)payload % 16 == 0);
+  p->aligned[0] = a0 ? 1 : 0;
+  p->aligned[1] = 1;
+  for (int b = 0; b < 2; ++b) {
+    p->segs[b] = reinterpret_cast<Seg *>(base + L.segs[b]);
+    p->tilemap[b] = reinterpret_cast<uint32_t *>(base + L.tilemap[b]);
+    p->lookback[b] = reinterpret_cast<u64 *>(base + L.lookback[b]);
+  }
+  p->smalls = reinterpret_cast<SmallSeg *>(base + L.smalls);
+  p->runs = reinterpret_cast<Run *>(base + L.runs);
+  p->chunkmap = reinterpret_cast<uint32_t *>(base + L.chunkmap);
+  p->seg_cap = L.seg_cap;
+  p->tile_cap = L.tile_cap;
+  p->small_cap = L.small_cap;
+  p->run_cap = L.run_cap;
+  p->chunk_cap = L.chunk_cap;
+  p->ctl = ws->d_ctl;
+  p->max_depth = 96;
+  p->fast_paths = 1;
+  p->mitigation = 1;
+  p->dran = 1.0;
+  p->small_t = kSmallT;
+}
+
+tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
+  KernelSet ks;
+  if (!get_set(kt, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
+  tsq_status st = prepare_small_smem(ks);
+  if (st != TSQ_OK) return st;
+  for (int i = 0; i < 4; ++i) TSQ_CUDA(cudaEventCreate(&ge->ev[i]));
+  TSQ_CUDA(cudaGraphCreate(&ge->graph, 0));
+  cudaGraph_t g = ge->graph;
+  cudaGraphNode_t e0, e1, e2, e3, cnode, lnode, snode, rnode;
+  TSQ_CUDA(cudaGraphAddEventRecordNode(&e0, g, nullptr, 0, ge->ev[0]));
+
+  static Params dummy;  // replaced per call via cudaGraphExecKernelNodeSetParams
+  memset(&dummy, 0, sizeof(dummy));
+  static Params *dummy_dst = nullptr;
+  dummy_dst = ws->d_params;
+  ge->init_params = cudaKernelNodeParams{};
+  void *init_args[2] = {&dummy, &dummy_dst};
+  ge->init_params.func = const_cast<void *>(ks.init);
+  ge->init_params.gridDim = dim3(1);
+  ge->init_params.blockDim = dim3(kThreads);
+  ge->init_params.sharedMemBytes = 0;
+  ge->init_params.kernelParams = init_args;
+  TSQ_CUDA(cudaGraphAddKernelNode(&ge->init_node, g, &e0, 1, &ge->init_params));
+  TSQ_CUDA(cudaGraphAddEventRecordNode(&e1, g, &ge->init_node, 1, ge->ev[1]));
+
+  TSQ_CUDA(cudaGraphConditionalHandleCreate(&ge->cond, g, 0, cudaGraphCondAssignDefault));
+  // cudaGraphNodeParams has a deleted default constructor (union member)
+  alignas(cudaGraphNodeParams) unsigned char cp_raw[sizeof(cudaGraphNodeParams)];
+  memset(cp_raw, 0, sizeof(cp_raw));
+  cudaGraphNodeParams &cp = *reinterpret_cast<cudaGraphNodeParams *>(cp_raw);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = ge->cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  TSQ_CUDA(cudaGraphAddNode(&cnode, g, &e1, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+
+  Params *dp = ws->d_params;
+  void *dev_args[1] = {&dp};
+  cudaKernelNodeParams lk;
+  lk = cudaKernelNodeParams{};
+  lk.func = const_cast<void *>(ks.level);
+  lk.gridDim = dim3(occupancy_grid(ws, ks.level, 0));
+  lk.blockDim = dim3(kThreads);
+  lk.kernelParams = dev_args;
+  TSQ_CUDA(cudaGraphAddKernelNode(&lnode, body, nullptr, 0, &lk));
+  TSQ_CUDA(cudaGraphAddEventRecordNode(&e2, g, &cnode, 1, ge->ev[2]));
+
+  cudaKernelNodeParams sk = lk;
+  sk.func = const_cast<void *>(ks.small);
+  sk.gridDim = dim3(occupancy_grid(ws, ks.small, ks.small_smem));
+  sk.sharedMemBytes = (unsigned)ks.small_smem;
+  TSQ_CUDA(cudaGraphAddKernelNode(&snode, g, &e2, 1, &sk));
+  cudaKernelNodeParams rk = lk;
+  rk.func = const_cast<void *>(ks.retire);
+  rk.gridDim = dim3(occupancy_grid(ws, ks.retire, 0));
+  TSQ_CUDA(cudaGraphAddKernelNode(&rnode, g, &e2, 1, &rk));
+  cudaGraphNode_t tail[2] = {snode, rnode};
+  TSQ_CUDA(cudaGraphAddEventRecordNode(&e3, g, tail, 2, ge->ev[3]));
+  TSQ_CUDA(cudaGraphInstantiate(&ge->exec, g, 0));
+  return TSQ_OK;
+}
+
+tsq_status reserve_locked(tsq_workspace *ws, size_t n, int kt, int pt, int small_t = kSmallT) {
+  const Layout L = make_layout(n, kt, pt, small_t);
+  if (L.total <= ws->block_bytes) {
+    if (n > ws->cap_elems) ws->cap_elems = n;
+    return TSQ_OK;
+  }
+  if (ws->block) {
+    cudaFree(ws->block);
+    ws->block = nullptr;
+    ws->block_bytes = 0;
+    ws->cap_elems = 0;
+  }
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, L.total);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return TSQ_ERR_ALLOC;
+  }
+  ws->block = p;
+  ws->block_bytes = L.total;
+  ws->cap_elems = n;
+  ws->alloc_count += 1;
+  return TSQ_OK;
+}
+
+tsq_status check_args(size_t n, int kt, int pt) {
+  if (key_bytes_of(kt) == 0) return TSQ_ERR_UNSUPPORTED_DTYPE;
+  if (pt != TSQ_NONE && pt != TSQ_U32) return TSQ_ERR_UNSUPPORTED_DTYPE;
+  if (n >= (1ull << 31)) return TSQ_ERR_INVALID;
+  return TSQ_OK;
+}
+
+tsq_status read_ctl(tsq_workspace *ws, cudaStream_t s) {
+  TSQ_CUDA(cudaMemcpyAsync(ws->h_ctl, ws->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+  TSQ_CUDA(cudaStreamSynchronize(s));
+  return TSQ_OK;
+}
+
+tsq_status fill_stats(tsq_workspace *ws, size_t n, tsq_stats *st) {
+  const Ctl &c = *ws->h_ctl;
+  memset(st, 0, sizeof(*st));
+  st->n = n;
+  st->stages = c.stages;
+  st->levels = c.levels;
+  st->max_depth = c.max_depth;
+  st->small_segments = c.small_count;
+  st->eq_runs = c.eq_runs;
+  st->eq_elements = c.eq_elements;
+  st->sorted_bypass = c.sorted_bypass;
+  st->reversed_bypass = c.reversed_bypass;
+  st->verify_fallbacks = c.verify_fallbacks;
+  st->partitioned_elements = c.partitioned_elements;
+  st->bytes_partition = c.bytes_partition;
+  st->bytes_small = c.bytes_small;
+  st->bytes_retire = c.bytes_retire;
+  st->temp_high_water = ws->cap_elems;
+  st->error_flags = c.error;
+  st->writes_caller = c.writes0;
+  st->writes_workspace = c.writes1;
+  if (c.error & ERR_DEPTH) return TSQ_ERR_DEPTH_EXCEEDED;
+  if (c.error) return TSQ_ERR_CAPACITY;
+  return TSQ_OK;
+}
+
+struct ActiveGuard {
+  tsq_workspace *ws;
+  explicit ActiveGuard(tsq_workspace *w) : ws(w) {}
+  ~ActiveGuard() {
+    std::lock_guard<std::mutex> lk(ws->mu);
+    ws->active = false;
+  }
+};
+
+tsq_status acquire(tsq_workspace *ws) {
+  std::lock_guard<std::mutex> lk(ws->mu);
+  if (ws->active) return TSQ_ERR_BUSY;
+  ws->active = true;
+  return TSQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *tsq_status_str(tsq_status s) {
+  switch (s) {
+    case TSQ_OK: return "ok";
+    case TSQ_ERR_ALLOC: return "device workspace allocation failed";
+    case TSQ_ERR_UNSUPPORTED_DTYPE: return "unsupported dtype";
+    case TSQ_ERR_CUDA: return "CUDA error";
+    case TSQ_ERR_DEPTH_EXCEEDED: return "recursion depth guard exceeded";
+    case TSQ_ERR_INVALID: return "invalid argument";
+    case TSQ_ERR_BUSY: return "sorter instance is not reentrant";
+    case TSQ_ERR_CAPACITY: return "device queue capacity exceeded";
+  }
+  return "unknown status";
+}
+
+int tsq_abi_version(void) { return TSQ_ABI_VERSION; }
+
+tsq_status tsq_workspace_create(tsq_workspace **out, int device) {
+  if (!out) return TSQ_ERR_INVALID;
+  *out = nullptr;
+  TSQ_CUDA(cudaSetDevice(device));
+  tsq_workspace *ws = new tsq_workspace();
+  ws->device = device;
+  cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc(&ws->d_params, sizeof(Params)) != cudaSuccess ||
+      cudaMalloc(&ws->d_ctl, sizeof(Ctl)) != cudaSuccess ||
+      cudaMallocHost(&ws->h_ctl, sizeof(Ctl)) != cudaSuccess) {
+    cudaGetLastError();
+    tsq_workspace_destroy(ws);
+    return TSQ_ERR_ALLOC;
+  }
+  memset(ws->h_ctl, 0, sizeof(Ctl));
+  cudaMemset(ws->d_ctl, 0, sizeof(Ctl));
+  TSQ_CUDA(cudaEventCreateWithFlags(&ws->done, cudaEventDisableTiming));
+  *out = ws;
+  return TSQ_OK;
+}
+
+void tsq_workspace_destroy(tsq_workspace *ws) {
+  if (!ws) return;
+  cudaSetDevice(ws->device);
+  cudaDeviceSynchronize();
+  for (auto &kv : ws->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    for (auto e : kv.second.ev)
+      if (e) cudaEventDestroy(e);
+  }
+  if (ws->block) cudaFree(ws->block);
+  if (ws->d_params) cudaFree(ws->d_params);
+  if (ws->d_ctl) cudaFree(ws->d_ctl);
+  if (ws->h_ctl) cudaFreeHost(ws->h_ctl);
+  if (ws->done) cudaEventDestroy(ws->done);
+  delete ws;
+}
+
+size_t tsq_workspace_bytes(size_t n, tsq_dtype key_t, tsq_dtype payload_t) {
+  if (check_args(n, key_t, payload_t) != TSQ_OK) return 0;
+  return make_layout(n, key_t, payload_t).total;
+}
+
+tsq_status tsq_workspace_reserve(tsq_workspace *ws, size_t n, tsq_dtype key_t,
+                                 tsq_dtype payload_t) {
+  if (!ws) return TSQ_ERR_INVALID;
+  tsq_status st = check_args(n, key_t, payload_t);
+  if (st != TSQ_OK) return st;
+  st = acquire(ws);
+  if (st != TSQ_OK) return st;
+  ActiveGuard g(ws);
+  cudaSetDevice(ws->device);
+  return reserve_locked(ws, n, key_t, payload_t);
+}
+
+tsq_status tsq_workspace_free(tsq_workspace *ws) {
+  if (!ws) return TSQ_ERR_INVALID;
+  tsq_status st = acquire(ws);
+  if (st != TSQ_OK) return st;
+  ActiveGuard g(ws);
+  cudaSetDevice(ws->device);
+  if (ws->block) {
+    cudaEventSynchronize(ws->done);
+    cudaFree(ws->block);
+  }
+  ws->block = nullptr;
+  ws->block_bytes = 0;
+  ws->cap_elems = 0;
+  return TSQ_OK;
+}
+
+size_t tsq_workspace_capacity(const tsq_workspace *ws) { return ws ? ws->cap_elems : 0; }
+uint64_t tsq_workspace_alloc_count(const tsq_workspace *ws) { return ws ? ws->alloc_count : 0; }
+
+tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dtype payload_t,
+                    const tsq_params *params, tsq_workspace *ws, void *stream,
+                    tsq_stats *stats) {
+  if (!ws) return TSQ_ERR_INVALID;
+  tsq_status st = check_args(n, key_t, payload_t);
+  if (st != TSQ_OK) return st;
+  if ((payload_t == TSQ_U32) != (payload != nullptr)) return TSQ_ERR_INVALID;
+  if (n > 0 && !keys) return TSQ_ERR_INVALID;
+  st = acquire(ws);
+  if (st != TSQ_OK) return st;
+  ActiveGuard guard(ws);
+  TSQ_CUDA(cudaSetDevice(ws->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (n <= 1) {
+    if (stats) stats->n = n;
+    return TSQ_OK;
+  }
+  int small_t = kSmallT;
+  if (params && params->small_threshold > 0)
+    small_t = params->small_threshold < kSmallT ? params->small_threshold : kSmallT;
+  // allocation precedes any mutation (core.py:1599, TempAllocationError)
+  st = reserve_locked(ws, n, key_t, payload_t, small_t);
+  if (st != TSQ_OK) return st;
+  const bool pay = payload_t == TSQ_U32;
+  KernelSet ks;
+  if (!get_set(key_t, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
+  const Layout L = make_layout(n, key_t, payload_t, small_t);
+  Params pv;
+  fill_params(ws, L, &pv, keys, payload, n);
+  pv.small_t = small_t;
+  tsq_params defaults;
+  memset(&defaults, 0, sizeof(defaults));
+  defaults.mitigation = 1;
+  defaults.fast_paths = 1;
+  const tsq_params &pp = params ? *params : defaults;
+  pv.dran = pp.dran > 0.0 ? pp.dran : 1.0;
+  pv.mitigation = pp.mitigation;
+  pv.fast_paths = pp.fast_paths;
+  pv.max_depth = pp.max_depth > 0 ? pp.max_depth : 96;
+  TSQ_CUDA(cudaStreamWaitEvent(s, ws->done, 0));
+
+  const int gkey = key_t * 2 + (pay ? 1 : 0);
+  if (!pp.host_levels) {
+    GraphEntry &ge = ws->graphs[gkey];
+    if (!ge.exec) {
+      st = build_graph(ws, key_t, pay, &ge);
+      if (st != TSQ_OK) {
+        ws->graphs.erase(gkey);
+        return st;
+      }
+    }
+    pv.use_cond = 1;
+    pv.cond = ge.cond;
+    Params *dst = ws->d_params;
+    void *args[2] = {&pv, &dst};
+    cudaKernelNodeParams kp = ge.init_params;
+    kp.kernelParams = args;
+    TSQ_CUDA(cudaGraphExecKernelNodeSetParams(ge.exec, ge.init_node, &kp));
+    TSQ_CUDA(cudaGraphLaunch(ge.exec, s));
+    TSQ_CUDA(cudaEventRecord(ws->done, s));
+    if (stats) {
+      st = read_ctl(ws, s);
+      if (st != TSQ_OK) return st;
+      st = fill_stats(ws, n, stats);
+      cudaEventElapsedTime(&stats->ms_levels, ge.ev[1], ge.ev[2]);
+      cudaEventElapsedTime(&stats->ms_total, ge.ev[0], ge.ev[3]);
+      return st;
+    }
+    return TSQ_OK;
+  }
+
+  // host-driven levels: same kernels, one launch per level with a read-back
+  // of the queue size in between (per-level timing / trace)
+  st = prepare_small_smem(ks);
+  if (st != TSQ_OK) return st;
+  pv.use_cond = 0;
+  cudaEvent_t e0, e1, t0, t1;
+  TSQ_CUDA(cudaEventCreate(&e0));
+  TSQ_CUDA(cudaEventCreate(&e1));
+  TSQ_CUDA(cudaEventCreate(&t0));
+  TSQ_CUDA(cudaEventCreate(&t1));
+  ws->level_ms.clear();
+  ws->level_segs.clear();
+  ws->level_tiles.clear();
+  Params *dst = ws->d_params;
+  TSQ_CUDA(cudaEventRecord(t0, s));
+  void *iargs[2] = {&pv, &dst};
+  TSQ_CUDA(cudaLaunchKernel(ks.init, dim3(1), dim3(kThreads), iargs, 0, s));
+  void *largs[1] = {&dst};
+  const int lgrid = occupancy_grid(ws, ks.level, 0);
+  float total_levels = 0.f;
+  for (int lv = 0; lv < kMaxLevels; ++lv) {
+    st = read_ctl(ws, s);
+    if (st != TSQ_OK) return st;
+    if (ws->h_ctl->cur_nseg == 0 || ws->h_ctl->error) break;
+    ws->level_segs.push_back(ws->h_ctl->cur_nseg);
+    ws->level_tiles.push_back(ws->h_ctl->cur_ntiles);
+    TSQ_CUDA(cudaEventRecord(e0, s));
+    TSQ_CUDA(cudaLaunchKernel(ks.level, dim3(lgrid), dim3(kThreads), largs, 0, s));
+    TSQ_CUDA(cudaEventRecord(e1, s));
+    TSQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ws->level_ms.push_back(ms);
+    total_levels += ms;
+  }
+  TSQ_CUDA(cudaLaunchKernel(ks.small, dim3(occupancy_grid(ws, ks.small, ks.small_smem)),
+                            dim3(kThreads), largs, ks.small_smem, s));
+  TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
+                            largs, 0, s));
+  TSQ_CUDA(cudaEventRecord(t1, s));
+  TSQ_CUDA(cudaEventRecord(ws->done, s));
+  st = read_ctl(ws, s);
+  if (st == TSQ_OK && stats) {
+    st = fill_stats(ws, n, stats);
+    stats->ms_levels = total_levels;
+    cudaEventElapsedTime(&stats->ms_total, t0, t1);
+  } else if (st == TSQ_OK && ws->h_ctl->error) {
+    st = (ws->h_ctl->error & ERR_DEPTH) ? TSQ_ERR_DEPTH_EXCEEDED : TSQ_ERR_CAPACITY;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  return st;
+}
+
+int tsq_level_trace(const tsq_workspace *ws, float *ms, uint32_t *segs, uint32_t *tiles,
+                    int cap) {
+  if (!ws) return 0;
+  int n = (int)ws->level_ms.size();
+  for (int i = 0; i < n && i < cap; ++i) {
+    if (ms) ms[i] = ws->level_ms[i];
+    if (segs) segs[i] = ws->level_segs[i];
+    if (tiles) tiles[i] = ws->level_tiles[i];
+  }
+  return n;
+}
+
+tsq_status tsq_partition_segment(const void *keys, const void *payload, void *out_keys,
+                                 void *out_payload, size_t n, tsq_dtype key_t,
+                                 tsq_dtype payload_t, uint64_t pivot, tsq_workspace *ws,
+                                 void *stream, int64_t *new_l, int64_t *new_r) {
+  if (!ws || !new_l || !new_r) return TSQ_ERR_INVALID;
+  tsq_status st = check_args(n, key_t, payload_t);
+  if (st != TSQ_OK) return st;
+  const bool pay = payload_t == TSQ_U32;
+  if (pay != (payload != nullptr) || pay != (out_payload != nullptr)) return TSQ_ERR_INVALID;
+  if (n == 0) {
+    *new_l = -1;
+    *new_r = 0;
+    return TSQ_OK;
+  }
+  st = acquire(ws);
+  if (st != TSQ_OK) return st;
+  ActiveGuard guard(ws);
+  TSQ_CUDA(cudaSetDevice(ws->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  st = reserve_locked(ws, n, key_t, payload_t);
+  if (st != TSQ_OK) return st;
+  KernelSet ks;
+  if (!get_set(key_t, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
+  const Layout L = make_layout(n, key_t, payload_t);
+  Params pv;
+  fill_params(ws, L, &pv, out_keys, out_payload, n);
+  pv.keys[1] = const_cast<void *>(keys);
+  pv.pay[1] = reinterpret_cast<uint32_t *>(const_cast<void *>(payload));
+  pv.raw[1] = 1;
+  pv.aligned[1] = ((uintptr_t)keys % 16 == 0) && ((uintptr_t)payload % 16 == 0);
+  pv.single_stage = 1;
+  pv.given_pivot = host_enc(key_t, pivot);
+  pv.use_cond = 0;
+  TSQ_CUDA(cudaStreamWaitEvent(s, ws->done, 0));
+  Params *dst = ws->d_params;
+  void *iargs[2] = {&pv, &dst};
+  TSQ_CUDA(cudaLaunchKernel(ks.init, dim3(1), dim3(kThreads), iargs, 0, s));
+  void *largs[1] = {&dst};
+  TSQ_CUDA(cudaLaunchKernel(ks.level, dim3(occupancy_grid(ws, ks.level, 0)), dim3(kThreads),
+                            largs, 0, s));
+  TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
+                            largs, 0, s));
+  TSQ_CUDA(cudaEventRecord(ws->done, s));
+  st = read_ctl(ws, s);
+  if (st != TSQ_OK) return st;
+  if (ws->h_ctl->error) return TSQ_ERR_CAPACITY;
+  *new_l = (int64_t)ws->h_ctl->stage_lt - 1;
+  *new_r = (int64_t)n - (int64_t)ws->h_ctl->stage_gt;
+  return TSQ_OK;
+}
+
+tsq_status tsq_select_pivot(const void *keys, size_t n, tsq_dtype key_t, double dran,
+                            int32_t mitigation, tsq_workspace *ws, void *stream,
+                            uint64_t *pivot, int32_t *order_flag) {
+  if (!ws || !pivot || !order_flag) return TSQ_ERR_INVALID;
+  tsq_status st = check_args(n, key_t, TSQ_NONE);
+  if (st != TSQ_OK) return st;
+  if (n < 2) return TSQ_ERR_INVALID;
+  st = acquire(ws);
+  if (st != TSQ_OK) return st;
+  ActiveGuard guard(ws);
+  TSQ_CUDA(cudaSetDevice(ws->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  KernelSet ks;
+  if (!get_set(key_t, false, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
+  Params pv;
+  memset(&pv, 0, sizeof(pv));
+  pv.keys[0] = const_cast<void *>(keys);
+  pv.raw[0] = 1;
+  pv.n = (long long)n;
+  pv.dran = dran > 0.0 ? dran : 1.0;
+  pv.mitigation = mitigation;
+  pv.ctl = ws->d_ctl;
+  TSQ_CUDA(cudaStreamWaitEvent(s, ws->done, 0));
+  void *args[1] = {&pv};
+  TSQ_CUDA(cudaLaunchKernel(ks.selp, dim3(1), dim3(kThreads), args, 0, s));
+  TSQ_CUDA(cudaEventRecord(ws->done, s));
+  st = read_ctl(ws, s);
+  if (st != TSQ_OK) return st;
+  const int kb = key_bytes_of(key_t);
+  *pivot = kb == 4 ? (ws->h_ctl->stage_lt & 0xffffffffull) : ws->h_ctl->stage_lt;
+  *order_flag = (int32_t)(long long)ws->h_ctl->stage_gt;
+  return TSQ_OK;
+}
+
+}  // extern "C"

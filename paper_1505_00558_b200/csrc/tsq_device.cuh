@@ -1,0 +1,260 @@
+// tsq_device.cuh -- device-side building blocks of the B200 three-way
+// partition sort: key codecs, queue records, the control block, and the
+// CTA-wide pivot-sampling / sorting-network / look-back helpers.
+//
+// Reference path being accelerated (tsqsort 0.1.0,
+// /root/reference/pkg/src/tsqsort): Sorter._range (core.py:1643-1728),
+// select_pivot (pivot.py:205-248), _run_machine (core.py:198-984) and
+// insertion_sort (smallsort.py:12-47).  See DESIGN.md for the mapping.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tsq.h"
+
+namespace tsq {
+
+typedef unsigned long long u64;
+
+constexpr int kThreads = 256;        // every kernel: 8 warps per CTA
+constexpr int kSmallT = 4096;        // segments <= this finish on chip
+constexpr int kMaxSample = 1023;     // pivot sample size cap (2^10 - 1)
+constexpr int kRunChunk = 8192;      // elements per retire work item
+constexpr int kMaxLevels = 200;      // hard stop for the level loop
+
+constexpr u64 kFlagAgg = 1ull << 62;  // look-back: tile aggregate published
+constexpr u64 kFlagInc = 2ull << 62;  // look-back: inclusive prefix published
+constexpr u64 kValMask = (1ull << 62) - 1;
+
+enum SegKind : uint32_t { KIND_PARTITION = 0, KIND_VERIFY_ASC = 1, KIND_VERIFY_DESC = 2 };
+enum RunKind : uint32_t { RUN_EQ = 0, RUN_SORTED = 1, RUN_REVERSED = 2 };
+enum ErrFlag : uint32_t { ERR_DEPTH = 1u, ERR_CAPACITY = 2u, ERR_LEVELS = 4u };
+
+// A live segment of one level: [begin, end) of buffer `buf` (0 = the
+// caller's keys, 1 = the workspace partner), partitioned around `pivot`
+// (an encoded key) or verified sorted / reversed.
+struct Seg {
+  long long begin, end;
+  u64 pivot;
+  uint32_t tile_base, ntiles;
+  uint32_t buf, kind, depth, noverify;
+  uint32_t done, fail;
+};
+
+// A segment of <= kSmallT elements waiting for the on-chip sort.
+struct SmallSeg {
+  long long begin;
+  int len;
+  int buf;
+};
+
+// A finished run: an ==p block (fill / payload copy from the side buffer),
+// or a verified sorted / reversed segment that only needs moving to buffer 0.
+struct Run {
+  long long begin, len;
+  u64 pivot;
+  long long src;          // ==p runs: payload offset in side_pay
+  uint32_t kind, buf;
+  uint32_t chunk_base, nchunks;
+};
+
+// Control block (device memory; zeroed by the init kernel every sort).
+struct Ctl {
+  u64 next_packed;        // (segments << 32) | tiles appended for next level
+  u64 run_packed;         // (runs << 32) | chunks appended
+  uint32_t cur_nseg, cur_ntiles;
+  uint32_t level, tile_ticket;
+  uint32_t ctas_done, small_count;
+  uint32_t small_ticket, run_ticket;
+  uint32_t error, pad0;
+  u64 stages, max_depth, levels, eq_runs, eq_elements;
+  u64 sorted_bypass, reversed_bypass, verify_fallbacks;
+  u64 partitioned_elements, small_elements;
+  u64 bytes_partition, bytes_small, bytes_retire;
+  u64 stage_lt, stage_gt;   // single-stage / select-pivot results
+  u64 writes0, writes1;     // element writes into buffer 0 / workspace
+};
+
+// Everything a kernel needs; lives in device memory, written by the init
+// kernel from its by-value argument so the captured graph can be reused.
+struct Params {
+  void *keys[2];          // [0] caller's keys, [1] workspace partner
+  uint32_t *pay[2];       // same for the uint32 payload (records)
+  uint32_t *side_pay;     // ==p payloads staged during a partition pass
+  long long n;
+  double dran;
+  int mitigation, fast_paths, max_depth, use_cond;
+  int raw[2];             // buffer holds the caller's encoding (else ordered)
+  int aligned[2];         // buffer's key / payload pointers are 16B aligned
+  int single_stage;       // tsq_partition_segment: one given-pivot stage
+  int small_t;            // segments <= small_t go to the on-chip sort
+  u64 given_pivot;        // encoded pivot for single_stage
+  Seg *segs[2];
+  uint32_t *tilemap[2];
+  u64 *lookback[2];
+  SmallSeg *smalls;
+  Run *runs;
+  uint32_t *chunkmap;
+  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap, pad1;
+  Ctl *ctl;
+  cudaGraphConditionalHandle cond;
+};
+
+// ---- order-preserving key codecs (native order -> unsigned order) ----------
+template <int DT> struct Codec;
+template <> struct Codec<TSQ_I32> {
+  typedef uint32_t U;
+  static __device__ __forceinline__ U enc(U x) { return x ^ 0x80000000u; }
+  static __device__ __forceinline__ U dec(U x) { return x ^ 0x80000000u; }
+};
+template <> struct Codec<TSQ_U32> {
+  typedef uint32_t U;
+  static __device__ __forceinline__ U enc(U x) { return x; }
+  static __device__ __forceinline__ U dec(U x) { return x; }
+};
+template <> struct Codec<TSQ_F32> {
+  typedef uint32_t U;
+  static __device__ __forceinline__ U enc(U x) {
+    return x ^ ((0u - (x >> 31)) | 0x80000000u);
+  }
+  static __device__ __forceinline__ U dec(U x) {
+    return x ^ (((x >> 31) - 1u) | 0x80000000u);
+  }
+};
+template <> struct Codec<TSQ_I64> {
+  typedef u64 U;
+  static __device__ __forceinline__ U enc(U x) { return x ^ 0x8000000000000000ull; }
+  static __device__ __forceinline__ U dec(U x) { return x ^ 0x8000000000000000ull; }
+};
+template <> struct Codec<TSQ_U64> {
+  typedef u64 U;
+  static __device__ __forceinline__ U enc(U x) { return x; }
+  static __device__ __forceinline__ U dec(U x) { return x; }
+};
+template <> struct Codec<TSQ_F64> {
+  typedef u64 U;
+  static __device__ __forceinline__ U enc(U x) {
+    return x ^ ((0ull - (x >> 63)) | 0x8000000000000000ull);
+  }
+  static __device__ __forceinline__ U dec(U x) {
+    return x ^ (((x >> 63) - 1ull) | 0x8000000000000000ull);
+  }
+};
+
+template <typename U> struct KeyMax;
+template <> struct KeyMax<uint32_t> { static constexpr uint32_t v = 0xffffffffu; };
+template <> struct KeyMax<u64> { static constexpr u64 v = ~0ull; };
+
+// 16-byte vector of keys / matching payload vector
+template <typename U> struct Vec;
+template <> struct Vec<uint32_t> {
+  static constexpr int N = 4;
+  typedef uint4 K;
+  typedef uint4 P;
+};
+template <> struct Vec<u64> {
+  static constexpr int N = 2;
+  typedef ulonglong2 K;
+  typedef uint2 P;
+};
+
+__device__ __forceinline__ uint32_t ldcg(const uint32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ u64 ldcg(const u64 *p) { return __ldcg(p); }
+
+__device__ __forceinline__ u64 ld_volatile(const u64 *p) {
+  return *reinterpret_cast<const volatile u64 *>(p);
+}
+__device__ __forceinline__ void st_volatile(u64 *p, u64 v) {
+  *reinterpret_cast<volatile u64 *>(p) = v;
+}
+__device__ __forceinline__ uint32_t ld_volatile32(const uint32_t *p) {
+  return *reinterpret_cast<const volatile uint32_t *>(p);
+}
+
+__device__ __forceinline__ u64 warp_sum64(u64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- pivot sample size: ~sqrt(len), 2^k - 1 with k in [5, 10] -------------
+__device__ __forceinline__ int sample_count(long long len) {
+  int bits = 64 - __clzll((long long)len);
+  int k = (bits + 1) >> 1;
+  k = k < 5 ? 5 : (k > 10 ? 10 : k);
+  return (1 << k) - 1;
+}
+
+// ---- CTA-wide bitonic sorting network over s[0, P2) (P2 power of two) -------
+template <typename U>
+__device__ __forceinline__ void cta_bitonic(U *s, int P2) {
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (P2 >> 1); i += blockDim.x) {
+        int lo = ((i / j) * 2 * j) + (i % j);
+        int hi = lo + j;
+        bool up = (lo & k) == 0;
+        U a = s[lo], b = s[hi];
+        if ((a > b) == up) {
+          s[lo] = b;
+          s[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---- device pivot sampling (select_pivot analogue, pivot.py:205-248) --------
+// Median of S = sample_count(len) strided samples; the first, middle and last
+// positions are fixed anchors and interior positions are shifted by the
+// MitigationRng jitter (dran, pivot.py:223-237).  Also returns the order flag
+// of the samples in position order (+1 nondecreasing, -1 nonincreasing).
+// All threads of the CTA must call; `s` holds >= 1024 U of shared memory.
+template <class C>
+__device__ void cta_select_pivot(const typename C::U *data, bool encoded_src,
+                                 long long begin, long long len, double dran,
+                                 int mitigation, typename C::U *s,
+                                 typename C::U *pivot_out, int *flag_out) {
+  typedef typename C::U U;
+  const int S = sample_count(len);
+  const int P2 = S + 1;
+  const int midi = S >> 1;
+  const long long span = len - 1;
+  long long shift = 0;
+  if (mitigation) {
+    const double stride = (double)span / (double)(S - 1);
+    shift = (long long)floor((dran - 1.0) * stride * 0.5);
+  }
+  for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+    U v = KeyMax<U>::v;
+    if (i < S) {
+      long long pos = begin + ((long long)i * span) / (S - 1);
+      if (i != 0 && i != midi && i != S - 1) {
+        pos += shift;
+        pos = pos < begin ? begin : (pos > begin + span ? begin + span : pos);
+      }
+      v = ldcg(data + pos);
+      if (!encoded_src) v = C::enc(v);
+    }
+    s[i] = v;
+  }
+  __syncthreads();
+  bool asc = true, desc = true;
+  for (int i = threadIdx.x; i < S - 1; i += blockDim.x) {
+    U a = s[i], b = s[i + 1];
+    asc &= (a <= b);
+    desc &= (a >= b);
+  }
+  asc = __syncthreads_and(asc);
+  desc = __syncthreads_and(desc);
+  cta_bitonic(s, P2);
+  if (threadIdx.x == 0) {
+    *pivot_out = s[midi];
+    *flag_out = asc ? 1 : (desc ? -1 : 0);
+  }
+  __syncthreads();
+}
+
+}  // namespace tsq

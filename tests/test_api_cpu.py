@@ -1,0 +1,171 @@
+"""CPU-only checks of the product boundary: the C-ABI library loads and
+exports every symbol include/tsq.h declares, host-side API semantics
+(config validation, RNG, error mapping) -- no compute calls without a GPU."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1505_00558_b200 as T
+from paper_1505_00558_b200 import _native as N
+from paper_1505_00558_b200.build import LIB, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "tsq.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(tsq_[a-z_]+)\s*\(", text)))
+
+
+def test_library_builds_and_exports_header_symbols():
+    build()
+    assert os.path.exists(LIB)
+    lib = ctypes.CDLL(LIB)
+    declared = _header_functions()
+    assert len(declared) >= 12
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(N.EXPORTED_SYMBOLS)
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True,
+                         check=True).stdout
+    for name in declared:
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings_and_abi():
+    lib = N.lib()
+    assert lib.tsq_abi_version() == 1
+    assert N.status_str(N.TSQ_ERR_BUSY) == "sorter instance is not reentrant"
+    assert N.status_str(N.TSQ_OK) == "ok"
+
+
+def test_workspace_bytes_scales():
+    lib = N.lib()
+    a = lib.tsq_workspace_bytes(1 << 20, N.TSQ_I32, N.TSQ_NONE)
+    b = lib.tsq_workspace_bytes(1 << 24, N.TSQ_I32, N.TSQ_NONE)
+    c = lib.tsq_workspace_bytes(1 << 20, N.TSQ_U64, N.TSQ_U32)
+    assert 4 << 20 <= a < 6 << 20       # one n*4 partner + small queues
+    assert 64 << 20 <= b < 80 << 20
+    assert c >= (1 << 20) * 16          # keys partner + payload partner + side buffer
+    assert lib.tsq_workspace_bytes(1 << 20, 99, 0) == 0
+
+
+def test_abi_struct_sizes_match_header():
+    # tsq_params: 8 + 6*4 + 3*8 ; tsq_stats: 18 u64 + 2 floats
+    assert ctypes.sizeof(N.TsqParams) == 56
+    assert ctypes.sizeof(N.TsqStats) == 18 * 8 + 8
+
+
+def test_sortconfig_validation_matches_reference():
+    # reference config.py:28-42
+    with pytest.raises(ValueError):
+        T.SortConfig(insertion_threshold=2)
+    with pytest.raises(ValueError):
+        T.SortConfig(medof3_max_n=700)
+    with pytest.raises(ValueError):
+        T.SortConfig(reverse_tolerance=-1)
+    with pytest.raises(ValueError):
+        T.SortConfig(late_swap_byte_threshold=0)
+    T.SortConfig(insertion_threshold=3)
+    with pytest.raises(ValueError):
+        T.GpuConfig(small_threshold=0)
+    with pytest.raises(ValueError):
+        T.GpuConfig(max_depth=4)
+
+
+def test_rng_matches_reference_kats():
+    r = T.MitigationRng(1)
+    T.rng_next(r)
+    assert r.zgen == 16807
+    T.rng_next(r)
+    assert r.zgen == 282475249
+    for _ in range(100):
+        T.rng_next(r)
+        assert 0.5 <= r.dran < 1.5 and r.dran2 == 1 + r.dran
+    assert T.MitigationRng(0).zgen != 0
+
+
+def test_rng_matches_golden():
+    from conftest import load_golden
+    for case in load_golden("rng.json"):
+        r = T.MitigationRng(case["seed"])
+        for zgen, dran, dran2 in case["seq"]:
+            r.next()
+            assert (r.zgen, r.dran, r.dran2) == (zgen, dran, dran2)
+
+
+def test_registry_signature():
+    fn = T.get_algorithm("tristate")
+    assert fn is T.REGISTRY["tristate"]
+    with pytest.raises(KeyError):
+        T.get_algorithm("nope")
+
+
+def test_trivial_inputs_need_no_device():
+    # n <= 1 returns before touching CUDA (core.py:1592-1593 semantics)
+    for ar in ([], [7]):
+        got = list(ar)
+        st = T.Sorter().sort_with_stats(got)
+        assert got == ar and st.comparisons == 0 and st.element_writes == 0
+
+
+def test_rejects_custom_comparator_and_late_swap_without_fallback():
+    with pytest.raises(TypeError):
+        T.Sorter().sort([3, 1, 2], cmp=lambda a, b: (a > b) - (a < b))
+    with pytest.raises(NotImplementedError):
+        T.Sorter().sort([3, 1, 2], element_size=400)
+    with pytest.raises(TypeError):
+        T.Sorter().sort(["a", "b", "c"])
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        T.Sorter().sort([3, 1, 2])
+
+
+def test_reentrancy_flag():
+    s = T.Sorter()
+    s._active = True
+    with pytest.raises(RuntimeError, match="not reentrant"):
+        s.sort([2, 1])
+    with pytest.raises(RuntimeError):
+        s.free_temp_storage()
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1505_00558_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in text.replace("oracle/", "").lower() or f == "core.py" \
+                    and "import oracle" not in text, f
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "tsq_oracle" not in text, f
+
+
+def test_workloads_generators_small():
+    import workloads as W
+    for fam in W.FAMILIES:
+        k, p = W.generate(fam, 4096)
+        assert k.size == 4096
+        assert (p is None) == (not W.FAMILIES[fam][1])
+    k, _ = W.generate("normal_f64", 100000)
+    assert not np.isnan(k).any() and not (np.signbit(k) & (k == 0)).any()
