@@ -214,8 +214,13 @@ class Sorter:
     # -- internals --
 
     def _device(self) -> int:
-        self.temp.workspace()
-        return self.temp.device
+        dev = getattr(self.temp, "device", None)
+        if dev is None:
+            torch = _torch()
+            if not torch.cuda.is_available():
+                raise RuntimeError("no CUDA device: the B200 sort has no CPU fallback")
+            dev = torch.cuda.current_device()
+        return dev
 
     def _stage(self, host, slot: str):
         """Device copy of a host tensor through a retained staging buffer."""

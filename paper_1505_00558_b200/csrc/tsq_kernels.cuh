@@ -406,7 +406,25 @@ __device__ void finalize_segment(const Params *P, Shared &sh, Seg *sgp, int cur,
       ctl->stage_gt = (u64)gt;
     }
   }
-  if (eq > 0) append_run(P, sh, RUN_EQ, sg.begin + lt, eq, sg.buf, sg.pivot, sg.begin);
+  if (eq > 0) {
+    if (PAY) {
+      // Records: the ==p payloads were staged at side_pay[begin ...], a
+      // range the children reuse at the next level, so they move to their
+      // final place now.  Nothing else touches [begin+lt, end-gt) of
+      // buffer 0 during this level: the segment's reads are complete and
+      // its < / > writes land outside the ==p block.
+      const uint32_t *side = P->side_pay + sg.begin;
+      uint32_t *p0 = P->pay[0] + sg.begin + lt;
+      U *k0 = reinterpret_cast<U *>(P->keys[0]) + sg.begin + lt;
+      const U v = P->raw[0] ? C::dec((U)sg.pivot) : (U)sg.pivot;
+      for (long long i = threadIdx.x; i < eq; i += kThreads) {
+        p0[i] = __ldcg(side + i);
+        k0[i] = v;
+      }
+    } else {
+      append_run(P, sh, RUN_EQ, sg.begin + lt, eq, sg.buf, sg.pivot, sg.begin);
+    }
+  }
   if (P->single_stage) return;
   const uint32_t db = sg.buf ^ 1u;
   const long long cb[2] = {sg.begin, sg.end - gt};
