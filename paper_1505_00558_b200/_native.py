@@ -98,6 +98,7 @@ def lib():
                                        ctypes.POINTER(ctypes.c_int32)]
         L.tsq_select_pivot.restype = i32
         L.tsq_level_trace.argtypes = [vp, ctypes.POINTER(ctypes.c_float),
+                                      ctypes.POINTER(ctypes.c_float),
                                       ctypes.POINTER(ctypes.c_uint32),
                                       ctypes.POINTER(ctypes.c_uint32), i32]
         L.tsq_level_trace.restype = i32
@@ -149,8 +150,10 @@ class Workspace:
     def level_trace(self):
         cap = 512
         ms = (ctypes.c_float * cap)()
+        sms = (ctypes.c_float * cap)()
         segs = (ctypes.c_uint32 * cap)()
         tiles = (ctypes.c_uint32 * cap)()
-        n = lib().tsq_level_trace(self.handle, ms, segs, tiles, cap)
+        n = lib().tsq_level_trace(self.handle, ms, sms, segs, tiles, cap)
         n = min(n, cap)
-        return [{"ms": ms[i], "segments": segs[i], "tiles": tiles[i]} for i in range(n)]
+        return [{"ms": ms[i], "sched_ms": sms[i], "segments": segs[i], "tiles": tiles[i]}
+                for i in range(n)]

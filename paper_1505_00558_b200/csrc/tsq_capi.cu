@@ -18,23 +18,27 @@ using namespace tsq;
 namespace {
 
 struct KernelSet {
-  const void *init, *level, *small, *retire, *selp;
+  const void *init, *part, *sched, *small, *retire, *selp;
   int key_bytes, tile;
-  size_t small_smem;
+  size_t part_smem, sched_smem, small_smem;
 };
 
 template <int DT, bool PAY>
 KernelSet make_set() {
   typedef Codec<DT> C;
+  typedef typename C::U U;
   KernelSet s;
   s.init = reinterpret_cast<const void *>(&init_kernel<C, PAY>);
-  s.level = reinterpret_cast<const void *>(&level_kernel<C, PAY>);
+  s.part = reinterpret_cast<const void *>(&partition_kernel<C, PAY>);
+  s.sched = reinterpret_cast<const void *>(&schedule_kernel<C, PAY>);
   s.small = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY>);
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
-  s.key_bytes = (int)sizeof(typename C::U);
+  s.key_bytes = (int)sizeof(U);
   s.tile = Geo<C, PAY>::TILE;
-  s.small_smem = (size_t)kSmallT * (sizeof(typename C::U) + (PAY ? 6 : 0));
+  s.part_smem = Geo<C, PAY>::SMEM;
+  s.sched_smem = (size_t)(kThreads / 32) * (kMaxSample + 1) * sizeof(U);
+  s.small_smem = (size_t)kSmallT * (sizeof(U) + (PAY ? 6 : 0));
   return s;
 }
 
@@ -140,7 +144,7 @@ struct tsq_workspace {
   bool active = false;
   std::mutex mu;
   std::map<int, GraphEntry> graphs;
-  std::vector<float> level_ms;      // host_levels mode trace
+  std::vector<float> level_ms, sched_ms;  // host_levels mode trace
   std::vector<uint32_t> level_segs, level_tiles;
 };
 
@@ -156,19 +160,42 @@ struct tsq_workspace {
 
 namespace {
 
-int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem) {
+int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem, int block = kThreads) {
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem) != cudaSuccess ||
       occ < 1)
     occ = 1;
   return occ * ws->num_sms;
 }
 
 tsq_status prepare_small_smem(const KernelSet &ks) {
-  if (ks.small_smem > 48 * 1024)
-    TSQ_CUDA(cudaFuncSetAttribute(ks.small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ks.small_smem));
+  const void *fns[3] = {ks.part, ks.sched, ks.small};
+  const size_t sm[3] = {ks.part_smem, ks.sched_smem, ks.small_smem};
+  for (int i = 0; i < 3; ++i)
+    if (sm[i] > 48 * 1024)
+      TSQ_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sm[i]));
   return TSQ_OK;
+}
+
+// one recursion level = partition pass + segment scheduling
+struct LevelLaunch {
+  dim3 part_grid, sched_grid;
+};
+
+LevelLaunch level_launch(tsq_workspace *ws, const KernelSet &ks) {
+  LevelLaunch L;
+  L.part_grid = dim3(occupancy_grid(ws, ks.part, ks.part_smem, kPartThreads));
+  L.sched_grid = dim3(occupancy_grid(ws, ks.sched, ks.sched_smem));
+  return L;
+}
+
+cudaError_t launch_level(const KernelSet &ks, const LevelLaunch &L, Params **dst,
+                         cudaStream_t s) {
+  void *args[1] = {dst};
+  cudaError_t e = cudaLaunchKernel(ks.part, L.part_grid, dim3(kPartThreads), args, ks.part_smem, s);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernel(ks.sched, L.sched_grid, dim3(kThreads), args, ks.sched_smem, s);
 }
 
 void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void *payload,
@@ -246,13 +273,22 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
 
   Params *dp = ws->d_params;
   void *dev_args[1] = {&dp};
-  cudaKernelNodeParams lk;
-  lk = cudaKernelNodeParams{};
-  lk.func = const_cast<void *>(ks.level);
-  lk.gridDim = dim3(occupancy_grid(ws, ks.level, 0));
+  const LevelLaunch LL = level_launch(ws, ks);
+  cudaKernelNodeParams pk = cudaKernelNodeParams{};
+  pk.func = const_cast<void *>(ks.part);
+  pk.gridDim = LL.part_grid;
+  pk.blockDim = dim3(kPartThreads);
+  pk.sharedMemBytes = (unsigned)ks.part_smem;
+  pk.kernelParams = dev_args;
+  TSQ_CUDA(cudaGraphAddKernelNode(&lnode, body, nullptr, 0, &pk));
+  cudaKernelNodeParams lk = cudaKernelNodeParams{};
+  lk.func = const_cast<void *>(ks.sched);
+  lk.gridDim = LL.sched_grid;
   lk.blockDim = dim3(kThreads);
+  lk.sharedMemBytes = (unsigned)ks.sched_smem;
   lk.kernelParams = dev_args;
-  TSQ_CUDA(cudaGraphAddKernelNode(&lnode, body, nullptr, 0, &lk));
+  cudaGraphNode_t schednode;
+  TSQ_CUDA(cudaGraphAddKernelNode(&schednode, body, &lnode, 1, &lk));
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e2, g, &cnode, 1, ge->ev[2]));
 
   cudaKernelNodeParams sk = lk;
@@ -263,6 +299,7 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   cudaKernelNodeParams rk = lk;
   rk.func = const_cast<void *>(ks.retire);
   rk.gridDim = dim3(occupancy_grid(ws, ks.retire, 0));
+  rk.sharedMemBytes = 0;
   TSQ_CUDA(cudaGraphAddKernelNode(&rnode, g, &e2, 1, &rk));
   cudaGraphNode_t tail[2] = {snode, rnode};
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e3, g, tail, 2, ge->ev[3]));
@@ -522,12 +559,14 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   st = prepare_small_smem(ks);
   if (st != TSQ_OK) return st;
   pv.use_cond = 0;
-  cudaEvent_t e0, e1, t0, t1;
+  cudaEvent_t e0, em, e1, t0, t1;
   TSQ_CUDA(cudaEventCreate(&e0));
+  TSQ_CUDA(cudaEventCreate(&em));
   TSQ_CUDA(cudaEventCreate(&e1));
   TSQ_CUDA(cudaEventCreate(&t0));
   TSQ_CUDA(cudaEventCreate(&t1));
   ws->level_ms.clear();
+  ws->sched_ms.clear();
   ws->level_segs.clear();
   ws->level_tiles.clear();
   Params *dst = ws->d_params;
@@ -535,7 +574,7 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   void *iargs[2] = {&pv, &dst};
   TSQ_CUDA(cudaLaunchKernel(ks.init, dim3(1), dim3(kThreads), iargs, 0, s));
   void *largs[1] = {&dst};
-  const int lgrid = occupancy_grid(ws, ks.level, 0);
+  const LevelLaunch LL = level_launch(ws, ks);
   float total_levels = 0.f;
   for (int lv = 0; lv < kMaxLevels; ++lv) {
     st = read_ctl(ws, s);
@@ -544,13 +583,17 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     ws->level_segs.push_back(ws->h_ctl->cur_nseg);
     ws->level_tiles.push_back(ws->h_ctl->cur_ntiles);
     TSQ_CUDA(cudaEventRecord(e0, s));
-    TSQ_CUDA(cudaLaunchKernel(ks.level, dim3(lgrid), dim3(kThreads), largs, 0, s));
+    TSQ_CUDA(cudaLaunchKernel(ks.part, LL.part_grid, dim3(kPartThreads), largs, ks.part_smem, s));
+    TSQ_CUDA(cudaEventRecord(em, s));
+    TSQ_CUDA(cudaLaunchKernel(ks.sched, LL.sched_grid, dim3(kThreads), largs, ks.sched_smem, s));
     TSQ_CUDA(cudaEventRecord(e1, s));
     TSQ_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
+    float ms = 0.f, ms2 = 0.f;
+    cudaEventElapsedTime(&ms, e0, em);
+    cudaEventElapsedTime(&ms2, em, e1);
     ws->level_ms.push_back(ms);
-    total_levels += ms;
+    ws->sched_ms.push_back(ms2);
+    total_levels += ms + ms2;
   }
   TSQ_CUDA(cudaLaunchKernel(ks.small, dim3(occupancy_grid(ws, ks.small, ks.small_smem)),
                             dim3(kThreads), largs, ks.small_smem, s));
@@ -567,18 +610,20 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     st = (ws->h_ctl->error & ERR_DEPTH) ? TSQ_ERR_DEPTH_EXCEEDED : TSQ_ERR_CAPACITY;
   }
   cudaEventDestroy(e0);
+  cudaEventDestroy(em);
   cudaEventDestroy(e1);
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
   return st;
 }
 
-int tsq_level_trace(const tsq_workspace *ws, float *ms, uint32_t *segs, uint32_t *tiles,
-                    int cap) {
+int tsq_level_trace(const tsq_workspace *ws, float *part_ms, float *sched_ms, uint32_t *segs,
+                    uint32_t *tiles, int cap) {
   if (!ws) return 0;
   int n = (int)ws->level_ms.size();
   for (int i = 0; i < n && i < cap; ++i) {
-    if (ms) ms[i] = ws->level_ms[i];
+    if (part_ms) part_ms[i] = ws->level_ms[i];
+    if (sched_ms) sched_ms[i] = ws->sched_ms[i];
     if (segs) segs[i] = ws->level_segs[i];
     if (tiles) tiles[i] = ws->level_tiles[i];
   }
@@ -623,8 +668,9 @@ tsq_status tsq_partition_segment(const void *keys, const void *payload, void *ou
   void *iargs[2] = {&pv, &dst};
   TSQ_CUDA(cudaLaunchKernel(ks.init, dim3(1), dim3(kThreads), iargs, 0, s));
   void *largs[1] = {&dst};
-  TSQ_CUDA(cudaLaunchKernel(ks.level, dim3(occupancy_grid(ws, ks.level, 0)), dim3(kThreads),
-                            largs, 0, s));
+  st = prepare_small_smem(ks);
+  if (st != TSQ_OK) return st;
+  TSQ_CUDA(launch_level(ks, level_launch(ws, ks), &dst, s));
   TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
                             largs, 0, s));
   TSQ_CUDA(cudaEventRecord(ws->done, s));
