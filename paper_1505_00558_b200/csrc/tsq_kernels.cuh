@@ -36,9 +36,12 @@ namespace tsq {
 
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;   // 256
-constexpr int kPartThreads = kConsumers + 32;     // + 1 producer warp
+constexpr int kProducerWarp = kConsumerWarps;     // warp 8: tile claims + bulk loads
+constexpr int kCounterWarp = kConsumerWarps + 1;  // warp 9: counts + look-back
+constexpr int kPartThreads = kConsumers + 64;
 constexpr int kStages = 3;                        // input ring depth
 constexpr int kAlign = 4;                         // bulk-copy element alignment
+constexpr int kOutPad = 16;                       // alignment slack of the out buffer
 constexpr uint32_t kDone = 0xffffffffu;
 
 template <class C, bool PAY>
@@ -50,7 +53,9 @@ struct Geo {
   static constexpr int TILE = kConsumers * IPT;
   static constexpr size_t KB = sizeof(U);
   static constexpr size_t STAGE_BYTES = (size_t)TILE * (KB + (PAY ? 4 : 0));
-  static constexpr size_t SMEM = (size_t)(kStages + 1) * STAGE_BYTES;
+  static constexpr size_t OUT_K = (size_t)(TILE + kOutPad) * KB;
+  static constexpr size_t OUT_P = PAY ? (size_t)(TILE + kOutPad) * 4 : 0;
+  static constexpr size_t SMEM = (size_t)kStages * STAGE_BYTES + OUT_K + OUT_P;
 };
 
 __device__ __forceinline__ void unpack(const uint4 &v, uint32_t *o) {
@@ -63,10 +68,12 @@ __device__ __forceinline__ void unpack(const uint2 &v, uint32_t *o) {
   o[0] = v.x; o[1] = v.y;
 }
 
-// Tile descriptor handed from the producer warp to the consumers.
+// Tile descriptor handed from the producer warp to the counter and consumer
+// warps; `excl` (the tile's exclusive (<, >) prefix in its segment) is filled
+// in by the counter warp.
 struct StageMeta {
   long long tstart, lo, hi, begin, end;
-  u64 pivot, next_key;
+  u64 pivot, next_key, excl;
   uint32_t t, k, kind, buf, tile_base, sid, skip, has_next;
 };
 
@@ -170,18 +177,25 @@ __device__ typename C::U warp_select_pivot(const typename C::U *data, bool encod
     const double stride = (double)span / (double)(S - 1);
     shift = (long long)floor((dran - 1.0) * stride * 0.5);
   }
-  for (int i = lane; i < P2; i += 32) {
-    U v = KeyMax<U>::v;
+  // all of a lane's sample loads are issued before any is consumed
+  U vals[(kMaxSample + 1) / 32];
+#pragma unroll
+  for (int q = 0; q < (kMaxSample + 1) / 32; ++q) {
+    const int i = lane + 32 * q;
+    vals[q] = KeyMax<U>::v;
     if (i < S) {
       long long pos = begin + ((long long)i * span) / (S - 1);
       if (i != 0 && i != midi && i != S - 1) {
         pos += shift;
         pos = pos < begin ? begin : (pos > begin + span ? begin + span : pos);
       }
-      v = ldcg(data + pos);
-      if (!encoded_src) v = C::enc(v);
+      vals[q] = ldcg(data + pos);
     }
-    s[i] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < (kMaxSample + 1) / 32; ++q) {
+    const int i = lane + 32 * q;
+    if (i < P2) s[i] = (i < S && !encoded_src) ? C::enc(vals[q]) : vals[q];
   }
   __syncwarp();
   bool asc = true, desc = true;
@@ -213,327 +227,25 @@ __device__ typename C::U warp_select_pivot(const typename C::U *data, bool encod
   return piv;
 }
 
-// ---------------------------------------------------------------------------
-// Partition kernel: producer warp.
+}  // namespace tsq
 
-template <class C, bool PAY>
-__device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t ntiles,
-                                              typename C::U *in_k, uint32_t *in_p, u64 *full,
-                                              u64 *empty, StageMeta *meta) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
-  const int lane = threadIdx.x & 31;
-  Ctl *ctl = P->ctl;
-  for (uint32_t it = 0;; ++it) {
-    const int s = (int)(it % kStages);
-    const uint32_t j = it / kStages;
-    if (j > 0) mbar_wait(&empty[s], (j - 1) & 1u);
-    uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(&ctl->tile_ticket, 1u);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    StageMeta &m = meta[s];
-    if (t >= ntiles) {
-      if (lane == 0) {
-        m.t = kDone;
-        mbar_arrive(&full[s]);
-      }
-      return;
-    }
-    const uint32_t sid = P->tilemap[cur][t];
-    const Seg *sgp = &P->segs[cur][sid];
-    const long long begin = sgp->begin, end = sgp->end;
-    const uint32_t tile_base = sgp->tile_base, kind = sgp->kind, buf = sgp->buf;
-    const uint32_t k = t - tile_base;
-    const long long tstart = (begin / G::TILE + k) * (long long)G::TILE;
-    const long long lo = tstart > begin ? tstart : begin;
-    const long long hi = (tstart + G::TILE) < end ? (tstart + G::TILE) : end;
-    const U *src = reinterpret_cast<const U *>(P->keys[buf]);
-    const uint32_t *psrc = PAY ? P->pay[buf] : nullptr;
-    U *dk = in_k + (size_t)s * G::TILE;
-    uint32_t *dp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
-    uint32_t skip = 0;
-    if (kind != KIND_PARTITION) skip = ld_volatile32(&sgp->fail) != 0 ? 1u : 0u;
-    uint32_t tx = 0;
-    long long a0 = 0, a1 = 0;
-    if (!skip) {
-      if (P->aligned[buf]) {
-        a0 = lo & ~(long long)(kAlign - 1);
-        a1 = (hi + kAlign - 1) & ~(long long)(kAlign - 1);
-        const long long cap = P->n & ~(long long)(kAlign - 1);  // never read past n
-        if (a1 > cap) a1 = cap;
-        if (a1 < a0) a1 = a0;
-        // ragged tail of the caller's array: plain loads
-        for (long long i = a1 + lane; i < hi; i += 32) {
-          dk[i - tstart] = src[i];
-          if (PAY) dp[i - tstart] = psrc[i];
-        }
-        tx = (uint32_t)((a1 - a0) * (long long)(sizeof(U) + (PAY ? 4 : 0)));
-      } else {
-        for (long long i = lo + lane; i < hi; i += 32) {
-          dk[i - tstart] = src[i];
-          if (PAY) dp[i - tstart] = psrc[i];
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      m.tstart = tstart; m.lo = lo; m.hi = hi; m.begin = begin; m.end = end;
-      m.pivot = sgp->pivot;
-      m.t = t; m.k = k; m.kind = kind; m.buf = buf; m.tile_base = tile_base; m.sid = sid;
-      m.skip = skip;
-      m.has_next = 0;
-      if (kind != KIND_PARTITION && !skip && hi < end) {
-        U v = src[hi];
-        if (P->raw[buf]) v = C::enc(v);
-        m.next_key = (u64)v;
-        m.has_next = 1;
-      }
-      if (tx) {
-        mbar_arrive_expect_tx(&full[s], tx);
-        bulk_load(dk + (a0 - tstart), src + a0, (uint32_t)((a1 - a0) * sizeof(U)), &full[s]);
-        if (PAY) bulk_load(dp + (a0 - tstart), psrc + a0, (uint32_t)((a1 - a0) * 4), &full[s]);
-      } else {
-        mbar_arrive(&full[s]);
-      }
-    }
-  }
-}
+#include "tsq_partition.cuh"
 
-// ---------------------------------------------------------------------------
-// Partition kernel: one tile on the consumer warps.
-
-template <class C, bool PAY>
-__device__ __forceinline__ void consume_partition(const Params *P, int cur, const StageMeta &m,
-                                                  const typename C::U *sk,
-                                                  const uint32_t *sp, u64 *empty_s,
-                                                  typename C::U *ok, uint32_t *op,
-                                                  uint32_t (*wcnt)[3], u64 *s_excl) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int sb = (int)m.buf, db = sb ^ 1;
-  const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
-  const U piv = (U)m.pivot;
-  const long long rlo = m.lo - m.tstart, rhi = m.hi - m.tstart;
-
-  U key[G::IPT];
-  uint32_t pay[PAY ? G::IPT : 1];
-  uint32_t cls[G::IPT];
-#pragma unroll
-  for (int v = 0; v < G::VPT; ++v) {
-    const int e0 = (v * kConsumers + tid) * G::VN;
-    typename Vec<U>::K kv = *reinterpret_cast<const typename Vec<U>::K *>(sk + e0);
-    unpack(kv, key + v * G::VN);
-    if (PAY) {
-      typename Vec<U>::P pv = *reinterpret_cast<const typename Vec<U>::P *>(sp + e0);
-      unpack(pv, pay + v * G::VN);
-    }
-#pragma unroll
-    for (int q = 0; q < G::VN; ++q) {
-      const int idx = e0 + q;
-      cls[v * G::VN + q] = (idx >= rlo && idx < rhi) ? 0u : 3u;
-    }
-  }
-  // the stage is in registers: hand it back to the producer
-  __syncwarp();
-  if (lane == 0) mbar_arrive(empty_s);
-#pragma unroll
-  for (int i = 0; i < G::IPT; ++i) {
-    if (src_raw) key[i] = C::enc(key[i]);
-    if (cls[i] == 0) cls[i] = key[i] < piv ? 0u : (key[i] == piv ? 1u : 2u);
-  }
-  // warp-level ranks per class, ordered by (item, lane)
-  const uint32_t lmask = (1u << lane) - 1u;
-  uint32_t lt_run = 0, gt_run = 0, eq_run = 0;
-  uint32_t rank[G::IPT];
-#pragma unroll
-  for (int i = 0; i < G::IPT; ++i) {
-    const uint32_t blt = __ballot_sync(0xffffffffu, cls[i] == 0);
-    const uint32_t bgt = __ballot_sync(0xffffffffu, cls[i] == 2);
-    const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, cls[i] == 1) : 0u;
-    uint32_t r;
-    if (cls[i] == 0) r = lt_run + __popc(blt & lmask);
-    else if (cls[i] == 2) r = gt_run + __popc(bgt & lmask);
-    else r = eq_run + __popc(beq & lmask);
-    rank[i] = r;
-    lt_run += __popc(blt);
-    gt_run += __popc(bgt);
-    eq_run += __popc(beq);
-  }
-  if (lane == 0) {
-    wcnt[warp][0] = lt_run;
-    wcnt[warp][1] = eq_run;
-    wcnt[warp][2] = gt_run;
-  }
-  named_sync(1, kConsumers);
-  uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
-#pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) {
-    const uint32_t a = wcnt[w][0], b = wcnt[w][1], c = wcnt[w][2];
-    if (w < warp) { w_lt += a; w_eq += b; w_gt += c; }
-    t_lt += a; t_eq += b; t_gt += c;
-  }
-  const u64 agg = ((u64)t_lt << 31) | (u64)t_gt;
-  u64 *lb = P->lookback[cur];
-  if (tid == 0) st_volatile(&lb[m.t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
-
-  // stage the tile as [< | > | == (payload only)]
-  const uint32_t nlg = t_lt + t_gt;
-#pragma unroll
-  for (int i = 0; i < G::IPT; ++i) {
-    const uint32_t c = cls[i];
-    if (c == 3u) continue;
-    uint32_t pos;
-    if (c == 0u) pos = w_lt + rank[i];
-    else if (c == 2u) pos = t_lt + w_gt + rank[i];
-    else {
-      if (!PAY) continue;
-      pos = nlg + w_eq + rank[i];
-    }
-    if (c != 1u) ok[pos] = key[i];
-    if (PAY) op[pos] = pay[i];
-  }
-
-  // decoupled look-back (warp 0), bounded by the segment's first tile
-  if (warp == 0) {
-    u64 excl = 0;
-    if (m.k > 0) {
-      long long base = (long long)m.t - 1;
-      const long long stop = (long long)m.tile_base;
-      for (;;) {
-        const long long idx = base - lane;
-        u64 d = kFlagInc;
-        if (idx >= stop) {
-          do {
-            d = ld_volatile(&lb[idx]);
-          } while ((d >> 62) == 0);
-        }
-        const uint32_t inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
-        if (inc) {
-          const int first = __ffs(inc) - 1;
-          excl += warp_sum64(lane <= first ? (d & kValMask) : 0ull);
-          break;
-        }
-        excl += warp_sum64(d & kValMask);
-        base -= 32;
-      }
-      if (lane == 0) st_volatile(&lb[m.t], kFlagInc | (excl + agg));
-    }
-    if (lane == 0) *s_excl = excl;
-  }
-  named_sync(1, kConsumers);
-
-  const u64 ex = *s_excl;
-  const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
-  U *dst = reinterpret_cast<U *>(P->keys[db]);
-  uint32_t *dpay = PAY ? P->pay[db] : nullptr;
-  const long long lt_base = m.begin + ex_lt;
-  const long long gt_base = m.end - 1 - ex_gt;
-  for (uint32_t i = tid; i < nlg; i += kConsumers) {
-    const long long d = (i < t_lt) ? (lt_base + i) : (gt_base - (long long)(i - t_lt));
-    U v = ok[i];
-    if (dst_raw) v = C::dec(v);
-    dst[d] = v;
-    if (PAY) dpay[d] = op[i];
-  }
-  if (PAY) {
-    const long long ex_eq = (m.lo - m.begin) - ex_lt - ex_gt;
-    uint32_t *side = P->side_pay + m.begin + ex_eq;
-    for (uint32_t i = tid; i < t_eq; i += kConsumers) side[i] = op[nlg + i];
-  }
-}
-
-// one verification tile: every adjacent pair inside the tile and the pair
-// that crosses into the next tile must be ordered; a violation marks the
-// segment failed (its later tiles are skipped by the producer)
-template <class C, bool PAY>
-__device__ __forceinline__ void consume_verify(const Params *P, int cur, const StageMeta &m,
-                                               const typename C::U *sk, u64 *empty_s,
-                                               uint32_t *s_flag) {
-  typedef typename C::U U;
-  const int tid = threadIdx.x;
-  const bool raw = P->raw[m.buf] != 0;
-  const bool asc = m.kind == KIND_VERIFY_ASC;
-  const long long rlo = m.lo - m.tstart, rhi = m.hi - m.tstart;
-  bool bad = false;
-  if (!m.skip) {
-    for (long long i = rlo + tid; i < rhi; i += kConsumers) {
-      U a = sk[i];
-      U b;
-      bool have = true;
-      if (i + 1 < rhi) b = sk[i + 1];
-      else if (m.has_next) b = (U)m.next_key;
-      else have = false;
-      if (raw) {
-        a = C::enc(a);
-        if (i + 1 < rhi) b = C::enc(b);
-      }
-      if (have) bad |= asc ? (a > b) : (a < b);
-    }
-  }
-  if (tid == 0) *s_flag = 0;
-  named_sync(1, kConsumers);
-  if (bad) *s_flag = 1;
-  __syncwarp();
-  if ((tid & 31) == 0) mbar_arrive(empty_s);
-  named_sync(1, kConsumers);
-  if (tid == 0 && *s_flag) atomicOr(&P->segs[cur][m.sid].fail, 1u);
-}
-
-template <class C, bool PAY>
-__global__ void __launch_bounds__(kPartThreads, PAY ? 2 : 3)
-    partition_kernel(const Params *__restrict__ P) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  U *in_k = reinterpret_cast<U *>(smem_raw);
-  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)kStages * G::TILE);
-  U *out_k = reinterpret_cast<U *>(smem_raw + (size_t)kStages * G::STAGE_BYTES);
-  uint32_t *out_p = reinterpret_cast<uint32_t *>(out_k + G::TILE);
-  __shared__ __align__(8) u64 full[kStages], empty[kStages];
-  __shared__ StageMeta meta[kStages];
-  __shared__ uint32_t wcnt[kConsumerWarps][3];
-  __shared__ u64 s_excl;
-  __shared__ uint32_t s_flag;
-
-  Ctl *ctl = P->ctl;
-  const uint32_t level = ctl->level;
-  const int cur = (int)(level & 1u);
-  const uint32_t ntiles = ctl->cur_ntiles;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (threadIdx.x >= kConsumers) {
-    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
-    return;
-  }
-  for (uint32_t it = 0;; ++it) {
-    const int s = (int)(it % kStages);
-    mbar_wait(&full[s], (it / kStages) & 1u);
-    const StageMeta m = meta[s];
-    if (m.t == kDone) break;
-    const U *sk = in_k + (size_t)s * G::TILE;
-    if (m.kind == KIND_PARTITION) {
-      consume_partition<C, PAY>(P, cur, m, sk, in_p + (size_t)s * G::TILE, &empty[s], out_k,
-                                out_p, wcnt, &s_excl);
-    } else {
-      consume_verify<C, PAY>(P, cur, m, sk, &empty[s], &s_flag);
-    }
-  }
-}
+namespace tsq {
 
 // ---------------------------------------------------------------------------
 // Schedule kernel: one warp per segment of the level just partitioned.
 
+// per-CTA statistics of the schedule kernel (shared-memory atomics, one
+// global flush per CTA instead of ~10 hot global atomics per segment)
+enum SchedStat {
+  ST_STAGES, ST_SORTED, ST_REVERSED, ST_DEPTH, ST_BYTES_PART, ST_BYTES_RETIRE, ST_W0, ST_W1,
+  ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_COUNT
+};
+
 template <class C, bool PAY>
 __device__ void schedule_segment(const Params *P, int cur, int nxt, uint32_t sid,
-                                 typename C::U *scratch) {
+                                 typename C::U *scratch, u64 *st) {
   typedef typename C::U U;
   const int lane = threadIdx.x & 31;
   Ctl *ctl = P->ctl;
@@ -546,18 +258,18 @@ __device__ void schedule_segment(const Params *P, int cur, int nxt, uint32_t sid
       const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
       const bool moves = !(rk == RUN_SORTED && sg.buf == 0);
       if (lane == 0) {
-        atomicAdd(&ctl->stages, 1ull);
-        atomicAdd(rk == RUN_SORTED ? &ctl->sorted_bypass : &ctl->reversed_bypass, 1ull);
-        atomicMax(&ctl->max_depth, (u64)sg.depth);
-        atomicAdd(&ctl->bytes_partition, (u64)len * kb);  // the verify read
+        atomicAdd(&st[ST_STAGES], 1ull);
+        atomicAdd(&st[rk == RUN_SORTED ? ST_SORTED : ST_REVERSED], 1ull);
+        atomicMax(&st[ST_DEPTH], (u64)sg.depth);
+        atomicAdd(&st[ST_BYTES_PART], (u64)len * kb);  // the verify read
         if (moves) {
-          atomicAdd(&ctl->bytes_retire, 2ull * (u64)len * (u64)(kb + (PAY ? 4 : 0)));
-          atomicAdd(&ctl->writes0, (u64)len);
+          atomicAdd(&st[ST_BYTES_RETIRE], 2ull * (u64)len * (u64)(kb + (PAY ? 4 : 0)));
+          atomicAdd(&st[ST_W0], (u64)len);
         }
       }
       if (moves) warp_append_run(P, rk, sg.begin, len, sg.buf, 0ull, sg.begin);
     } else {
-      if (lane == 0) atomicAdd(&ctl->verify_fallbacks, 1ull);
+      if (lane == 0) atomicAdd(&st[ST_FALLBACK], 1ull);
       warp_append_level<C, PAY>(P, nxt, sg.begin, sg.end, sg.buf, sg.pivot, KIND_PARTITION,
                                 sg.depth, 1);
     }
@@ -568,19 +280,19 @@ __device__ void schedule_segment(const Params *P, int cur, int nxt, uint32_t sid
   const long long gt = (long long)(inc & 0x7fffffffull);
   const long long eq = len - lt - gt;
   if (lane == 0) {
-    atomicAdd(&ctl->stages, 1ull);
-    atomicAdd(&ctl->partitioned_elements, (u64)len);
-    atomicMax(&ctl->max_depth, (u64)sg.depth);
+    atomicAdd(&st[ST_STAGES], 1ull);
+    atomicAdd(&st[ST_PARTITIONED], (u64)len);
+    atomicMax(&st[ST_DEPTH], (u64)sg.depth);
     u64 bytes = (u64)len * kb + (u64)(lt + gt) * kb;
     if (PAY) bytes += (u64)len * 8ull;
-    atomicAdd(&ctl->bytes_partition, bytes);
-    atomicAdd(sg.buf == 0 ? &ctl->writes1 : &ctl->writes0, (u64)(lt + gt));
-    if (PAY) atomicAdd(&ctl->writes1, (u64)eq);
+    atomicAdd(&st[ST_BYTES_PART], bytes);
+    atomicAdd(&st[sg.buf == 0 ? ST_W1 : ST_W0], (u64)(lt + gt));
+    if (PAY) atomicAdd(&st[ST_W1], (u64)eq);
     if (eq > 0) {
-      atomicAdd(&ctl->eq_runs, 1ull);
-      atomicAdd(&ctl->eq_elements, (u64)eq);
-      atomicAdd(&ctl->bytes_retire, (u64)eq * (kb + (PAY ? 8 : 0)));
-      atomicAdd(&ctl->writes0, (u64)eq);
+      atomicAdd(&st[ST_EQ_RUNS], 1ull);
+      atomicAdd(&st[ST_EQ_ELEMS], (u64)eq);
+      atomicAdd(&st[ST_BYTES_RETIRE], (u64)eq * (kb + (PAY ? 8 : 0)));
+      atomicAdd(&st[ST_W0], (u64)eq);
     }
     if (P->single_stage) {
       ctl->stage_lt = (u64)lt;
@@ -615,7 +327,7 @@ __device__ void schedule_segment(const Params *P, int cur, int nxt, uint32_t sid
     if (cl[c] <= P->small_t) {
       if (lane == 0) {
         append_small(P, cb[c], cl[c], db);
-        atomicMax(&ctl->max_depth, (u64)depth);
+        atomicMax(&st[ST_DEPTH], (u64)depth);
       }
       continue;
     }
@@ -648,11 +360,22 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
     for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < cap; i += gridDim.x * kThreads)
       lbn[i] = 0ull;
   }
+  __shared__ u64 st[ST_COUNT];
+  if (threadIdx.x < ST_COUNT) st[threadIdx.x] = 0ull;
+  __syncthreads();
   const uint32_t nwarps = gridDim.x * (kThreads / 32);
   for (uint32_t sid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); sid < nseg;
        sid += nwarps)
-    schedule_segment<C, PAY>(P, cur, nxt, sid, scratch);
+    schedule_segment<C, PAY>(P, cur, nxt, sid, scratch, st);
   __syncthreads();
+  if (threadIdx.x < ST_COUNT && st[threadIdx.x]) {
+    u64 *dst[ST_COUNT] = {&ctl->stages, &ctl->sorted_bypass, &ctl->reversed_bypass,
+                          &ctl->max_depth, &ctl->bytes_partition, &ctl->bytes_retire,
+                          &ctl->writes0, &ctl->writes1, &ctl->verify_fallbacks,
+                          &ctl->partitioned_elements, &ctl->eq_runs, &ctl->eq_elements};
+    if (threadIdx.x == ST_DEPTH) atomicMax(dst[ST_DEPTH], st[ST_DEPTH]);
+    else atomicAdd(dst[threadIdx.x], st[threadIdx.x]);
+  }
   if (threadIdx.x == 0) {
     __threadfence();
     const uint32_t d = atomicAdd(&ctl->ctas_done, 1u);

@@ -1,0 +1,426 @@
+// tsq_partition.cuh -- the multi-block three-way partition pass (one
+// recursion level over every live segment).  Included by tsq_kernels.cuh.
+//
+// The stage it performs is the one _run_machine performs for one segment
+// (/root/reference/pkg/src/tsqsort/core.py:198-984): afterwards every key
+// < p sits at the segment front, every key > p at the back, and the == p
+// block (retired, never compared again) in between (core.py:944-967).
+//
+// Persistent CTAs, warp-specialised (320 threads):
+//   warp 8  producer  claims tiles (one atomic ticket each, one claim ahead),
+//                     resolves their segment, and streams the tile into a
+//                     3-deep shared-memory ring with cp.async.bulk (TMA
+//                     engine) completing on the stage's mbarrier
+//   warp 9  counter   as soon as a stage lands: counts its < / > keys,
+//                     publishes the tile aggregate, resolves the tile's
+//                     exclusive prefix by decoupled look-back over the
+//                     segment's earlier tiles, publishes the inclusive
+//                     prefix and hands the offset to the consumers
+//   warps 0-7 consumers  classify every key against the pivot, rank it in
+//                     its class with __ballot_sync / __popc, stage the < run
+//                     and the > run (and, for records, the == payloads) in
+//                     shared memory aligned like their destinations, and
+//                     write them with cp.async.bulk stores (scalar stores for
+//                     the <= 3 unaligned keys at each end)
+#pragma once
+
+namespace tsq {
+
+// ---------------------------------------------------------------------------
+// Producer warp.
+
+template <class C, bool PAY>
+__device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t ntiles,
+                                              typename C::U *in_k, uint32_t *in_p, u64 *full,
+                                              u64 *empty, StageMeta *meta) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  const int lane = threadIdx.x & 31;
+  Ctl *ctl = P->ctl;
+  uint32_t t_next = 0;
+  if (lane == 0) t_next = atomicAdd(&ctl->tile_ticket, 1u);
+  for (uint32_t it = 0;; ++it) {
+    const int s = (int)(it % kStages);
+    const uint32_t j = it / kStages;
+    uint32_t t = __shfl_sync(0xffffffffu, t_next, 0);
+    StageMeta &m = meta[s];
+    if (t >= ntiles) {
+      if (j > 0) mbar_wait(&empty[s], (j - 1) & 1u);
+      if (lane == 0) {
+        m.t = kDone;
+        mbar_arrive(&full[s]);
+      }
+      return;
+    }
+    // claim the following tile now; its atomic overlaps this tile's work
+    if (lane == 0) t_next = atomicAdd(&ctl->tile_ticket, 1u);
+    const uint32_t sid = P->tilemap[cur][t];
+    const Seg *sgp = &P->segs[cur][sid];
+    const long long begin = sgp->begin, end = sgp->end;
+    const uint32_t tile_base = sgp->tile_base, kind = sgp->kind, buf = sgp->buf;
+    const u64 pivot = sgp->pivot;
+    const uint32_t k = t - tile_base;
+    const long long tstart = (begin / G::TILE + k) * (long long)G::TILE;
+    const long long lo = tstart > begin ? tstart : begin;
+    const long long hi = (tstart + G::TILE) < end ? (tstart + G::TILE) : end;
+    const U *src = reinterpret_cast<const U *>(P->keys[buf]);
+    const uint32_t *psrc = PAY ? P->pay[buf] : nullptr;
+    uint32_t skip = 0;
+    if (kind != KIND_PARTITION) skip = ld_volatile32(&sgp->fail) != 0 ? 1u : 0u;
+    if (j > 0) mbar_wait(&empty[s], (j - 1) & 1u);
+    U *dk = in_k + (size_t)s * G::TILE;
+    uint32_t *dp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
+    uint32_t tx = 0;
+    long long a0 = 0, a1 = 0;
+    if (!skip) {
+      if (P->aligned[buf]) {
+        a0 = lo & ~(long long)(kAlign - 1);
+        a1 = (hi + kAlign - 1) & ~(long long)(kAlign - 1);
+        const long long cap = P->n & ~(long long)(kAlign - 1);  // never read past n
+        if (a1 > cap) a1 = cap;
+        if (a1 < a0) a1 = a0;
+        for (long long i = a1 + lane; i < hi; i += 32) {  // ragged end of the array
+          dk[i - tstart] = src[i];
+          if (PAY) dp[i - tstart] = psrc[i];
+        }
+        tx = (uint32_t)((a1 - a0) * (long long)(sizeof(U) + (PAY ? 4 : 0)));
+      } else {
+        for (long long i = lo + lane; i < hi; i += 32) {
+          dk[i - tstart] = src[i];
+          if (PAY) dp[i - tstart] = psrc[i];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      m.tstart = tstart; m.lo = lo; m.hi = hi; m.begin = begin; m.end = end;
+      m.pivot = pivot;
+      m.t = t; m.k = k; m.kind = kind; m.buf = buf; m.tile_base = tile_base; m.sid = sid;
+      m.skip = skip;
+      m.has_next = 0;
+      if (kind != KIND_PARTITION && !skip && hi < end) {
+        U v = src[hi];
+        if (P->raw[buf]) v = C::enc(v);
+        m.next_key = (u64)v;
+        m.has_next = 1;
+      }
+      if (tx) {
+        mbar_arrive_expect_tx(&full[s], tx);
+        bulk_load(dk + (a0 - tstart), src + a0, (uint32_t)((a1 - a0) * sizeof(U)), &full[s]);
+        if (PAY) bulk_load(dp + (a0 - tstart), psrc + a0, (uint32_t)((a1 - a0) * 4), &full[s]);
+      } else {
+        mbar_arrive(&full[s]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Counter warp: tile aggregate + decoupled look-back, ahead of the consumers.
+
+template <class C, bool PAY>
+__device__ __forceinline__ void counter_loop(const Params *P, int cur, const typename C::U *in_k,
+                                             u64 *full, u64 *ready, u64 *empty,
+                                             StageMeta *meta) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  const int lane = threadIdx.x & 31;
+  u64 *lb = P->lookback[cur];
+  for (uint32_t it = 0;; ++it) {
+    const int s = (int)(it % kStages);
+    mbar_wait(&full[s], (it / kStages) & 1u);
+    StageMeta &m = meta[s];
+    const uint32_t t = m.t;
+    if (t == kDone) return;
+    if (m.kind == KIND_PARTITION) {
+      const U piv = (U)m.pivot;
+      const bool raw = P->raw[m.buf] != 0;
+      const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
+      const U *sk = in_k + (size_t)s * G::TILE;
+      uint32_t lt = 0, gt = 0;
+      const bool full_tile = rlo == 0 && rhi == G::TILE;
+#pragma unroll 4
+      for (int v = lane; v < G::TILE / G::VN; v += 32) {
+        U kk[G::VN];
+        unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + v * G::VN), kk);
+#pragma unroll
+        for (int q = 0; q < G::VN; ++q) {
+          const int idx = v * G::VN + q;
+          const U x = raw ? C::enc(kk[q]) : kk[q];
+          const bool ok = full_tile || (idx >= rlo && idx < rhi);
+          lt += (ok && x < piv) ? 1u : 0u;
+          gt += (ok && x > piv) ? 1u : 0u;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lt += __shfl_xor_sync(0xffffffffu, lt, o);
+        gt += __shfl_xor_sync(0xffffffffu, gt, o);
+      }
+      const u64 agg = ((u64)lt << 31) | (u64)gt;
+      u64 excl = 0;
+      if (m.k == 0) {
+        if (lane == 0) st_volatile(&lb[t], kFlagInc | agg);
+      } else {
+        if (lane == 0) st_volatile(&lb[t], kFlagAgg | agg);
+        long long base = (long long)t - 1;
+        const long long stop = (long long)m.tile_base;
+        for (;;) {
+          const long long idx = base - lane;
+          u64 d = kFlagInc;
+          if (idx >= stop) {
+            do {
+              d = ld_volatile(&lb[idx]);
+            } while ((d >> 62) == 0);
+          }
+          const uint32_t inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+          if (inc) {
+            const int first = __ffs(inc) - 1;
+            excl += warp_sum64(lane <= first ? (d & kValMask) : 0ull);
+            break;
+          }
+          excl += warp_sum64(d & kValMask);
+          base -= 32;
+        }
+        if (lane == 0) st_volatile(&lb[t], kFlagInc | (excl + agg));
+      }
+      if (lane == 0) m.excl = excl;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&ready[s]);
+      mbar_arrive(&empty[s]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Consumers.
+
+// Write one staged run: element j of the run (global index D + j) sits at
+// R[(D & 3) + j]; the 16B-aligned body goes out as one bulk store issued by
+// `issuer`, the <= 3 keys at each ragged end as scalar stores by `lane` < 8
+// of warp `scal_warp`.
+template <typename T>
+__device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T *R,
+                                         bool issuer, int scal_warp) {
+  if (L <= 0) return;
+  const long long b0 = (D + kAlign - 1) & ~(long long)(kAlign - 1);
+  const long long b1 = (D + L) & ~(long long)(kAlign - 1);
+  const long long base = D & ~(long long)(kAlign - 1);
+  const bool body = b1 > b0;
+  if (body && issuer)
+    bulk_store(g + b0, R + (b0 - base), (uint32_t)((b1 - b0) * (long long)sizeof(T)));
+  if ((int)(threadIdx.x >> 5) == scal_warp) {
+    const int lane = threadIdx.x & 31;
+    const long long h = body ? (b0 - D) : L;            // head count (all if no body)
+    const long long ts = body ? (b1 - D) : L;           // tail start
+    const long long e = lane < h ? lane : ts + (lane - h);
+    if (lane < 8 && (lane < h || e < L)) g[D + e] = R[(D - base) + e];
+  }
+}
+
+template <class C, bool PAY>
+__device__ __forceinline__ void consume_partition(const Params *P, const StageMeta *mp,
+                                                  const typename C::U *sk, const uint32_t *sp,
+                                                  u64 *ready_s, uint32_t ready_par,
+                                                  u64 *empty_s, typename C::U *ok,
+                                                  uint32_t *op, uint32_t (*wcnt)[3]) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const StageMeta m = *mp;
+  const int sb = (int)m.buf, db = sb ^ 1;
+  const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
+  const U piv = (U)m.pivot;
+  const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
+  const bool full_tile = rlo == 0 && rhi == G::TILE;
+
+  U key[G::IPT];
+  uint32_t pay[PAY ? G::IPT : 1];
+  uint32_t cls[G::IPT];  // class (0 <, 1 ==, 2 >, 3 none) << 16 | rank in class
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + tid) * G::VN;
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key + v * G::VN);
+    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay + v * G::VN);
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) {
+      const int idx = e0 + q;
+      cls[v * G::VN + q] = (full_tile || (idx >= rlo && idx < rhi)) ? 0u : 3u;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < G::IPT; ++i) {
+    if (src_raw) key[i] = C::enc(key[i]);
+    if (cls[i] == 0) cls[i] = key[i] < piv ? 0u : (key[i] == piv ? 1u : 2u);
+  }
+  // warp-level ranks per class, ordered by (item, lane)
+  const uint32_t lmask = (1u << lane) - 1u;
+  uint32_t lt_run = 0, gt_run = 0, eq_run = 0;
+#pragma unroll
+  for (int i = 0; i < G::IPT; ++i) {
+    const uint32_t blt = __ballot_sync(0xffffffffu, cls[i] == 0);
+    const uint32_t bgt = __ballot_sync(0xffffffffu, cls[i] == 2);
+    const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, cls[i] == 1) : 0u;
+    const uint32_t bm = cls[i] == 0 ? blt : (cls[i] == 2 ? bgt : beq);
+    const uint32_t base = cls[i] == 0 ? lt_run : (cls[i] == 2 ? gt_run : eq_run);
+    cls[i] = (cls[i] << 16) | (base + __popc(bm & lmask));
+    lt_run += __popc(blt);
+    gt_run += __popc(bgt);
+    eq_run += __popc(beq);
+  }
+  if (lane == 0) {
+    wcnt[warp][0] = lt_run;
+    wcnt[warp][1] = eq_run;
+    wcnt[warp][2] = gt_run;
+  }
+  // the previous tile's bulk stores must have finished reading the out
+  // buffer before it is restaged
+  if (tid == 0) bulk_wait_read0();
+  named_sync(1, kConsumers);
+  uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) {
+    const uint32_t a = wcnt[w][0], b = wcnt[w][1], c = wcnt[w][2];
+    if (w < warp) { w_lt += a; w_eq += b; w_gt += c; }
+    t_lt += a; t_eq += b; t_gt += c;
+  }
+  // the tile's offsets from the counter warp; then the stage can be reused
+  mbar_wait(ready_s, ready_par);
+  const u64 ex = mp->excl;
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_s);
+  const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
+  const long long D_lt = m.begin + ex_lt;                  // first slot of this tile's < run
+  const long long D_gt = m.end - ex_gt - (long long)t_gt;  // first slot of its > run
+  const long long ex_eq = (m.lo - m.begin) - ex_lt - ex_gt;
+  const long long D_eq = m.begin + ex_eq;                  // records: side buffer slot
+  const int o_lt = (int)(D_lt & (kAlign - 1));
+  const int g_base = (o_lt + (int)t_lt + kAlign - 1) & ~(kAlign - 1);
+  const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
+  const int e_base = (o_gt + (int)t_gt + kAlign - 1) & ~(kAlign - 1);
+  const int o_eq = e_base + (int)(D_eq & (kAlign - 1));
+#pragma unroll
+  for (int i = 0; i < G::IPT; ++i) {
+    const uint32_t c = cls[i] >> 16, rk = cls[i] & 0xffffu;
+    if (c == 3u) continue;
+    int pos;
+    if (c == 0u) pos = o_lt + (int)(w_lt + rk);
+    else if (c == 2u) pos = o_gt + (int)(t_gt - 1u - (w_gt + rk));  // > run fills backwards
+    else {
+      if (!PAY) continue;
+      pos = o_eq + (int)(w_eq + rk);
+    }
+    if (c != 1u) ok[pos] = dst_raw ? C::dec(key[i]) : key[i];
+    if (PAY) op[pos] = pay[i];
+  }
+  fence_proxy_async_smem();
+  named_sync(1, kConsumers);
+  U *dst = reinterpret_cast<U *>(P->keys[db]);
+  const bool issuer = tid == 0;
+  emit_run<U>(dst, D_lt, t_lt, ok, issuer, 1);
+  emit_run<U>(dst, D_gt, t_gt, ok + g_base, issuer, 2);
+  if (PAY) {
+    uint32_t *dpay = P->pay[db];
+    emit_run<uint32_t>(dpay, D_lt, t_lt, op, issuer, 3);
+    emit_run<uint32_t>(dpay, D_gt, t_gt, op + g_base, issuer, 4);
+    emit_run<uint32_t>(P->side_pay, D_eq, t_eq, op + e_base, issuer, 5);
+  }
+  if (issuer) bulk_commit();
+}
+
+// one verification tile: every adjacent pair inside the tile and the pair
+// that crosses into the next tile must be ordered; a violation marks the
+// segment failed (its later tiles are skipped by the producer)
+template <class C, bool PAY>
+__device__ __forceinline__ void consume_verify(const Params *P, int cur, const StageMeta &m,
+                                               const typename C::U *sk, u64 *empty_s,
+                                               uint32_t *s_flag) {
+  typedef typename C::U U;
+  const int tid = threadIdx.x;
+  const bool raw = P->raw[m.buf] != 0;
+  const bool asc = m.kind == KIND_VERIFY_ASC;
+  const long long rlo = m.lo - m.tstart, rhi = m.hi - m.tstart;
+  bool bad = false;
+  if (!m.skip) {
+    for (long long i = rlo + tid; i < rhi; i += kConsumers) {
+      U a = sk[i];
+      U b;
+      bool have = true;
+      if (i + 1 < rhi) b = sk[i + 1];
+      else if (m.has_next) b = (U)m.next_key;
+      else have = false;
+      if (raw) {
+        a = C::enc(a);
+        if (i + 1 < rhi) b = C::enc(b);
+      }
+      if (have) bad |= asc ? (a > b) : (a < b);
+    }
+  }
+  if (tid == 0) *s_flag = 0;
+  named_sync(1, kConsumers);
+  if (bad) *s_flag = 1;
+  __syncwarp();
+  if ((tid & 31) == 0) mbar_arrive(empty_s);
+  named_sync(1, kConsumers);
+  if (tid == 0 && *s_flag) atomicOr(&P->segs[cur][m.sid].fail, 1u);
+}
+
+template <class C, bool PAY>
+__global__ void __launch_bounds__(kPartThreads, PAY ? 2 : 3)
+    partition_kernel(const Params *__restrict__ P) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  U *in_k = reinterpret_cast<U *>(smem_raw);
+  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)kStages * G::TILE);
+  U *out_k = reinterpret_cast<U *>(smem_raw + (size_t)kStages * G::STAGE_BYTES);
+  uint32_t *out_p = reinterpret_cast<uint32_t *>(smem_raw + (size_t)kStages * G::STAGE_BYTES +
+                                                 G::OUT_K);
+  __shared__ __align__(8) u64 full[kStages], ready[kStages], empty[kStages];
+  __shared__ StageMeta meta[kStages];
+  __shared__ uint32_t wcnt[kConsumerWarps][3];
+  __shared__ uint32_t s_flag;
+
+  Ctl *ctl = P->ctl;
+  const uint32_t level = ctl->level;
+  const int cur = (int)(level & 1u);
+  const uint32_t ntiles = ctl->cur_ntiles;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], 1);
+      mbar_init(&empty[s], kConsumerWarps + 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  if (warp == kProducerWarp) {
+    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
+    return;
+  }
+  if (warp == kCounterWarp) {
+    counter_loop<C, PAY>(P, cur, in_k, full, ready, empty, meta);
+    return;
+  }
+  for (uint32_t it = 0;; ++it) {
+    const int s = (int)(it % kStages);
+    const uint32_t par = (it / kStages) & 1u;
+    mbar_wait(&full[s], par);
+    if (meta[s].t == kDone) break;
+    const U *sk = in_k + (size_t)s * G::TILE;
+    if (meta[s].kind == KIND_PARTITION) {
+      consume_partition<C, PAY>(P, &meta[s], sk, in_p + (size_t)s * G::TILE, &ready[s], par,
+                                &empty[s], out_k, out_p, wcnt);
+    } else {
+      const StageMeta m = meta[s];
+      consume_verify<C, PAY>(P, cur, m, sk, &empty[s], &s_flag);
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+}  // namespace tsq

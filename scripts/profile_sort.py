@@ -14,7 +14,7 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else (1 << 26)
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 keys, pay = W.generate(fam, n)
 src = torch.from_numpy(keys).cuda()
-s = T.Sorter(seed=1)
+s = T.Sorter(seed=1, gpu=T.GpuConfig(host_levels=os.environ.get("TSQ_HOST_LEVELS") == "1"))
 for _ in range(reps):
     d = src.clone()
     if pay is not None:
