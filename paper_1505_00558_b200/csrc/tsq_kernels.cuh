@@ -77,329 +77,12 @@ struct StageMeta {
   uint32_t t, k, kind, buf, tile_base, sid, skip, has_next;
 };
 
-// ---------------------------------------------------------------------------
-// Warp-level queue appends (lane 0 claims the slot; the warp fills the map).
-
-template <class C, bool PAY>
-__device__ void warp_append_level(const Params *P, int nxt, long long begin, long long end,
-                                  uint32_t buf, u64 pivot, uint32_t kind, uint32_t depth,
-                                  uint32_t noverify) {
-  const int lane = threadIdx.x & 31;
-  const long long T = Geo<C, PAY>::TILE;
-  const uint32_t ntiles = (uint32_t)((end - 1) / T - begin / T + 1);
-  uint32_t slot = kDone, tbase = 0;
-  if (lane == 0) {
-    Ctl *ctl = P->ctl;
-    const u64 old = atomicAdd(&ctl->next_packed, (1ull << 32) | ntiles);
-    slot = (uint32_t)(old >> 32);
-    tbase = (uint32_t)old;
-    if (slot < P->seg_cap && (u64)tbase + ntiles <= P->tile_cap) {
-      Seg s;
-      s.begin = begin; s.end = end; s.pivot = pivot;
-      s.tile_base = tbase; s.ntiles = ntiles;
-      s.buf = buf; s.kind = kind; s.depth = depth; s.noverify = noverify;
-      s.done = 0; s.fail = 0;
-      P->segs[nxt][slot] = s;
-    } else {
-      atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-      slot = kDone;
-    }
-  }
-  slot = __shfl_sync(0xffffffffu, slot, 0);
-  tbase = __shfl_sync(0xffffffffu, tbase, 0);
-  if (slot != kDone) {
-    uint32_t *tm = P->tilemap[nxt] + tbase;
-    for (uint32_t i = lane; i < ntiles; i += 32) tm[i] = slot;
-  }
-}
-
-__device__ void warp_append_run(const Params *P, uint32_t kind, long long begin, long long len,
-                                uint32_t buf, u64 pivot, long long src) {
-  const int lane = threadIdx.x & 31;
-  uint32_t nchunks;
-  if (kind == RUN_REVERSED && buf == 0)
-    nchunks = (uint32_t)(((len >> 1) + kRunChunk - 1) / kRunChunk);
-  else
-    nchunks = (uint32_t)((len + kRunChunk - 1) / kRunChunk);
-  if (nchunks == 0) return;
-  uint32_t slot = kDone, cbase = 0;
-  if (lane == 0) {
-    Ctl *ctl = P->ctl;
-    const u64 old = atomicAdd(&ctl->run_packed, (1ull << 32) | nchunks);
-    slot = (uint32_t)(old >> 32);
-    cbase = (uint32_t)old;
-    if (slot < P->run_cap && (u64)cbase + nchunks <= P->chunk_cap) {
-      Run r;
-      r.begin = begin; r.len = len; r.pivot = pivot; r.src = src;
-      r.kind = kind; r.buf = buf; r.chunk_base = cbase; r.nchunks = nchunks;
-      P->runs[slot] = r;
-    } else {
-      atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-      slot = kDone;
-    }
-  }
-  slot = __shfl_sync(0xffffffffu, slot, 0);
-  cbase = __shfl_sync(0xffffffffu, cbase, 0);
-  if (slot != kDone) {
-    uint32_t *cm = P->chunkmap + cbase;
-    for (uint32_t i = lane; i < nchunks; i += 32) cm[i] = slot;
-  }
-}
-
-__device__ __forceinline__ void append_small(const Params *P, long long begin, long long len,
-                                             uint32_t buf) {
-  Ctl *ctl = P->ctl;
-  const uint32_t slot = atomicAdd(&ctl->small_count, 1u);
-  if (slot < P->small_cap) {
-    SmallSeg s;
-    s.begin = begin; s.len = (int)len; s.buf = (int)buf;
-    P->smalls[slot] = s;
-  } else {
-    atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-  }
-}
-
-// ---- warp-level pivot sampling (select_pivot analogue, pivot.py:205-248) ---
-// Same sample positions as cta_select_pivot; `s` is this warp's scratch of
-// kMaxSample + 1 keys.  Returns the pivot; *flag gets the order flag.
-template <class C>
-__device__ typename C::U warp_select_pivot(const typename C::U *data, bool encoded_src,
-                                           long long begin, long long len, double dran,
-                                           int mitigation, typename C::U *s, int *flag) {
-  typedef typename C::U U;
-  const int lane = threadIdx.x & 31;
-  const int S = sample_count(len);
-  const int P2 = S + 1;
-  const int midi = S >> 1;
-  const long long span = len - 1;
-  long long shift = 0;
-  if (mitigation) {
-    const double stride = (double)span / (double)(S - 1);
-    shift = (long long)floor((dran - 1.0) * stride * 0.5);
-  }
-  // all of a lane's sample loads are issued before any is consumed
-  U vals[(kMaxSample + 1) / 32];
-#pragma unroll
-  for (int q = 0; q < (kMaxSample + 1) / 32; ++q) {
-    const int i = lane + 32 * q;
-    vals[q] = KeyMax<U>::v;
-    if (i < S) {
-      long long pos = begin + ((long long)i * span) / (S - 1);
-      if (i != 0 && i != midi && i != S - 1) {
-        pos += shift;
-        pos = pos < begin ? begin : (pos > begin + span ? begin + span : pos);
-      }
-      vals[q] = ldcg(data + pos);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < (kMaxSample + 1) / 32; ++q) {
-    const int i = lane + 32 * q;
-    if (i < P2) s[i] = (i < S && !encoded_src) ? C::enc(vals[q]) : vals[q];
-  }
-  __syncwarp();
-  bool asc = true, desc = true;
-  for (int i = lane; i < S - 1; i += 32) {
-    const U a = s[i], b = s[i + 1];
-    asc &= (a <= b);
-    desc &= (a >= b);
-  }
-  asc = __all_sync(0xffffffffu, asc);
-  desc = __all_sync(0xffffffffu, desc);
-  for (int k = 2; k <= P2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < (P2 >> 1); i += 32) {
-        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-        const int hi = lo + j;
-        const bool up = (lo & k) == 0;
-        const U a = s[lo], b = s[hi];
-        if ((a > b) == up) {
-          s[lo] = b;
-          s[hi] = a;
-        }
-      }
-      __syncwarp();
-    }
-  }
-  *flag = asc ? 1 : (desc ? -1 : 0);
-  const U piv = s[midi];
-  __syncwarp();
-  return piv;
-}
-
 }  // namespace tsq
 
 #include "tsq_partition.cuh"
+#include "tsq_schedule.cuh"
 
 namespace tsq {
-
-// ---------------------------------------------------------------------------
-// Schedule kernel: one warp per segment of the level just partitioned.
-
-// per-CTA statistics of the schedule kernel (shared-memory atomics, one
-// global flush per CTA instead of ~10 hot global atomics per segment)
-enum SchedStat {
-  ST_STAGES, ST_SORTED, ST_REVERSED, ST_DEPTH, ST_BYTES_PART, ST_BYTES_RETIRE, ST_W0, ST_W1,
-  ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_COUNT
-};
-
-template <class C, bool PAY>
-__device__ void schedule_segment(const Params *P, int cur, int nxt, uint32_t sid,
-                                 typename C::U *scratch, u64 *st) {
-  typedef typename C::U U;
-  const int lane = threadIdx.x & 31;
-  Ctl *ctl = P->ctl;
-  const Seg sg = P->segs[cur][sid];
-  const long long len = sg.end - sg.begin;
-  const int kb = (int)sizeof(U);
-  if (sg.kind != KIND_PARTITION) {
-    const bool failed = sg.fail != 0;
-    if (!failed) {
-      const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
-      const bool moves = !(rk == RUN_SORTED && sg.buf == 0);
-      if (lane == 0) {
-        atomicAdd(&st[ST_STAGES], 1ull);
-        atomicAdd(&st[rk == RUN_SORTED ? ST_SORTED : ST_REVERSED], 1ull);
-        atomicMax(&st[ST_DEPTH], (u64)sg.depth);
-        atomicAdd(&st[ST_BYTES_PART], (u64)len * kb);  // the verify read
-        if (moves) {
-          atomicAdd(&st[ST_BYTES_RETIRE], 2ull * (u64)len * (u64)(kb + (PAY ? 4 : 0)));
-          atomicAdd(&st[ST_W0], (u64)len);
-        }
-      }
-      if (moves) warp_append_run(P, rk, sg.begin, len, sg.buf, 0ull, sg.begin);
-    } else {
-      if (lane == 0) atomicAdd(&st[ST_FALLBACK], 1ull);
-      warp_append_level<C, PAY>(P, nxt, sg.begin, sg.end, sg.buf, sg.pivot, KIND_PARTITION,
-                                sg.depth, 1);
-    }
-    return;
-  }
-  const u64 inc = P->lookback[cur][sg.tile_base + sg.ntiles - 1];
-  const long long lt = (long long)((inc >> 31) & 0x7fffffffull);
-  const long long gt = (long long)(inc & 0x7fffffffull);
-  const long long eq = len - lt - gt;
-  if (lane == 0) {
-    atomicAdd(&st[ST_STAGES], 1ull);
-    atomicAdd(&st[ST_PARTITIONED], (u64)len);
-    atomicMax(&st[ST_DEPTH], (u64)sg.depth);
-    u64 bytes = (u64)len * kb + (u64)(lt + gt) * kb;
-    if (PAY) bytes += (u64)len * 8ull;
-    atomicAdd(&st[ST_BYTES_PART], bytes);
-    atomicAdd(&st[sg.buf == 0 ? ST_W1 : ST_W0], (u64)(lt + gt));
-    if (PAY) atomicAdd(&st[ST_W1], (u64)eq);
-    if (eq > 0) {
-      atomicAdd(&st[ST_EQ_RUNS], 1ull);
-      atomicAdd(&st[ST_EQ_ELEMS], (u64)eq);
-      atomicAdd(&st[ST_BYTES_RETIRE], (u64)eq * (kb + (PAY ? 8 : 0)));
-      atomicAdd(&st[ST_W0], (u64)eq);
-    }
-    if (P->single_stage) {
-      ctl->stage_lt = (u64)lt;
-      ctl->stage_gt = (u64)gt;
-    }
-  }
-  if (eq > 0) {
-    if (PAY) {
-      // Records: the ==p payloads sit at side_pay[begin ...], a range the
-      // children reuse at the next level, so they move to their final place
-      // now (nothing else touches [begin+lt, end-gt) of buffer 0).
-      const uint32_t *side = P->side_pay + sg.begin;
-      uint32_t *p0 = P->pay[0] + sg.begin + lt;
-      U *k0 = reinterpret_cast<U *>(P->keys[0]) + sg.begin + lt;
-      const U v = P->raw[0] ? C::dec((U)sg.pivot) : (U)sg.pivot;
-      for (long long i = lane; i < eq; i += 32) {
-        p0[i] = side[i];
-        k0[i] = v;
-      }
-    } else {
-      warp_append_run(P, RUN_EQ, sg.begin + lt, eq, sg.buf, sg.pivot, sg.begin);
-    }
-  }
-  if (P->single_stage) return;
-  const uint32_t db = sg.buf ^ 1u;
-  const long long cb[2] = {sg.begin, sg.end - gt};
-  const long long cl[2] = {lt, gt};
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    if (cl[c] <= 0) continue;
-    const uint32_t depth = sg.depth + 1;
-    if (cl[c] <= P->small_t) {
-      if (lane == 0) {
-        append_small(P, cb[c], cl[c], db);
-        atomicMax(&st[ST_DEPTH], (u64)depth);
-      }
-      continue;
-    }
-    if ((int)depth > P->max_depth) {
-      if (lane == 0) atomicOr(&ctl->error, (uint32_t)ERR_DEPTH);
-      continue;
-    }
-    int flag = 0;
-    const U piv = warp_select_pivot<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
-                                       cb[c], cl[c], P->dran, P->mitigation, scratch, &flag);
-    uint32_t kind = KIND_PARTITION;
-    if (P->fast_paths)
-      kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
-    warp_append_level<C, PAY>(P, nxt, cb[c], cb[c] + cl[c], db, (u64)piv, kind, depth, 0);
-  }
-}
-
-template <class C, bool PAY>
-__global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__restrict__ P) {
-  typedef typename C::U U;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  U *scratch = reinterpret_cast<U *>(smem_raw) + (threadIdx.x >> 5) * (kMaxSample + 1);
-  Ctl *ctl = P->ctl;
-  const uint32_t level = ctl->level;
-  const int cur = (int)(level & 1u), nxt = cur ^ 1;
-  const uint32_t nseg = ctl->cur_nseg;
-  {
-    u64 *lbn = P->lookback[nxt];
-    const uint32_t cap = P->tile_cap;
-    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < cap; i += gridDim.x * kThreads)
-      lbn[i] = 0ull;
-  }
-  __shared__ u64 st[ST_COUNT];
-  if (threadIdx.x < ST_COUNT) st[threadIdx.x] = 0ull;
-  __syncthreads();
-  const uint32_t nwarps = gridDim.x * (kThreads / 32);
-  for (uint32_t sid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); sid < nseg;
-       sid += nwarps)
-    schedule_segment<C, PAY>(P, cur, nxt, sid, scratch, st);
-  __syncthreads();
-  if (threadIdx.x < ST_COUNT && st[threadIdx.x]) {
-    u64 *dst[ST_COUNT] = {&ctl->stages, &ctl->sorted_bypass, &ctl->reversed_bypass,
-                          &ctl->max_depth, &ctl->bytes_partition, &ctl->bytes_retire,
-                          &ctl->writes0, &ctl->writes1, &ctl->verify_fallbacks,
-                          &ctl->partitioned_elements, &ctl->eq_runs, &ctl->eq_elements};
-    if (threadIdx.x == ST_DEPTH) atomicMax(dst[ST_DEPTH], st[ST_DEPTH]);
-    else atomicAdd(dst[threadIdx.x], st[threadIdx.x]);
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t d = atomicAdd(&ctl->ctas_done, 1u);
-    if (d == gridDim.x - 1) {
-      __threadfence();
-      const u64 packed = atomicExch(&ctl->next_packed, 0ull);
-      const uint32_t ns = (uint32_t)(packed >> 32), nt = (uint32_t)packed;
-      ctl->cur_nseg = ns;
-      ctl->cur_ntiles = nt;
-      ctl->tile_ticket = 0;
-      ctl->ctas_done = 0;
-      ctl->level = level + 1;
-      ctl->levels += 1;
-      bool more = ns > 0;
-      if (more && level + 1 >= (uint32_t)kMaxLevels) {
-        atomicOr(&ctl->error, (uint32_t)ERR_LEVELS);
-        more = false;
-      }
-      if (ctl->error) more = false;
-      __threadfence();
-      if (P->use_cond) cudaGraphSetConditional(P->cond, more ? 1u : 0u);
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 

@@ -237,24 +237,22 @@ __device__ __forceinline__ void consume_partition(const Params *P, const StageMe
   const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
   const bool full_tile = rlo == 0 && rhi == G::TILE;
 
-  U key[G::IPT];
-  uint32_t pay[PAY ? G::IPT : 1];
+  // keys stay in the shared-memory stage until they are staged for output;
+  // registers carry only (class << 16 | rank) per key
   uint32_t cls[G::IPT];  // class (0 <, 1 ==, 2 >, 3 none) << 16 | rank in class
 #pragma unroll
   for (int v = 0; v < G::VPT; ++v) {
     const int e0 = (v * kConsumers + tid) * G::VN;
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key + v * G::VN);
-    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay + v * G::VN);
+    U key[G::VN];
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) {
       const int idx = e0 + q;
-      cls[v * G::VN + q] = (full_tile || (idx >= rlo && idx < rhi)) ? 0u : 3u;
+      const U x = src_raw ? C::enc(key[q]) : key[q];
+      cls[v * G::VN + q] = (full_tile || (idx >= rlo && idx < rhi))
+                               ? (x < piv ? 0u : (x == piv ? 1u : 2u))
+                               : 3u;
     }
-  }
-#pragma unroll
-  for (int i = 0; i < G::IPT; ++i) {
-    if (src_raw) key[i] = C::enc(key[i]);
-    if (cls[i] == 0) cls[i] = key[i] < piv ? 0u : (key[i] == piv ? 1u : 2u);
   }
   // warp-level ranks per class, ordered by (item, lane)
   const uint32_t lmask = (1u << lane) - 1u;
@@ -290,8 +288,6 @@ __device__ __forceinline__ void consume_partition(const Params *P, const StageMe
   // the tile's offsets from the counter warp; then the stage can be reused
   mbar_wait(ready_s, ready_par);
   const u64 ex = mp->excl;
-  __syncwarp();
-  if (lane == 0) mbar_arrive(empty_s);
   const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
   const long long D_lt = m.begin + ex_lt;                  // first slot of this tile's < run
   const long long D_gt = m.end - ex_gt - (long long)t_gt;  // first slot of its > run
@@ -313,9 +309,17 @@ __device__ __forceinline__ void consume_partition(const Params *P, const StageMe
       if (!PAY) continue;
       pos = o_eq + (int)(w_eq + rk);
     }
-    if (c != 1u) ok[pos] = dst_raw ? C::dec(key[i]) : key[i];
-    if (PAY) op[pos] = pay[i];
+    const int e = ((i / G::VN) * kConsumers + tid) * G::VN + (i % G::VN);
+    if (c != 1u) {
+      U x = sk[e];
+      if (src_raw != dst_raw) x = src_raw ? C::enc(x) : C::dec(x);
+      ok[pos] = x;
+    }
+    if (PAY) op[pos] = sp[e];
   }
+  // the stage is no longer needed: hand it back to the producer
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_s);
   fence_proxy_async_smem();
   named_sync(1, kConsumers);
   U *dst = reinterpret_cast<U *>(P->keys[db]);
