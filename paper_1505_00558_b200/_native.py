@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsq_b200.so")
+LIB_PATH = os.environ.get("TSQ_LIB") or os.path.join(HERE, "libtsq_b200.so")
 
 TSQ_NONE, TSQ_I32, TSQ_U32, TSQ_I64, TSQ_U64, TSQ_F32, TSQ_F64 = range(7)
 

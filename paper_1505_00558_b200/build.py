@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtsq_b200.so")
+TRACE_LIB = os.path.join(HERE, "libtsq_b200_trace.so")  # profiling build (-DTSQ_TRACE)
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -32,26 +33,30 @@ def sources():
                   [os.path.join(ROOT, "include", "tsq.h")])
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    lib = TRACE_LIB if trace else LIB
+    if not force and up_to_date(lib):
+        return lib
     cmd = [nvcc_path(), ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-Wall", "-diag-suppress=177", "-shared", "-o", LIB + ".tmp",
+           "-Xcompiler", "-Wall", "-diag-suppress=177,1886", "-shared", "-o", lib + ".tmp",
            os.path.join(CSRC, "tsq_capi.cu")]
+    if trace:
+        cmd.insert(1, "-DTSQ_TRACE")
     if verbose:
         cmd.insert(5, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                trace="--trace" in sys.argv))

@@ -717,3 +717,22 @@ tsq_status tsq_select_pivot(const void *keys, size_t n, tsq_dtype key_t, double 
 }
 
 }  // extern "C"
+
+#ifdef TSQ_TRACE
+// Profiling builds only (libtsq_b200_trace.so): per-tile timeline of one
+// level of the partition pass, read back by scripts/trace_level.py.
+extern "C" int tsq_trace_set_level(int level) {
+  return cudaMemcpyToSymbol(tsq::g_trace_level, &level, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int tsq_trace_copy(void *dst, size_t bytes) {
+  const size_t cap = sizeof(tsq::g_trace);
+  if (bytes > cap) bytes = cap;
+  if (cudaMemset(nullptr, 0, 0) != cudaSuccess) cudaGetLastError();
+  return cudaMemcpyFromSymbol(dst, tsq::g_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+extern "C" int tsq_trace_clear(void) {
+  void *p = nullptr;
+  if (cudaGetSymbolAddress(&p, tsq::g_trace) != cudaSuccess) return -1;
+  return cudaMemset(p, 0, sizeof(tsq::g_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif

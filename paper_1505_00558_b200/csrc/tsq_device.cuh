@@ -101,6 +101,23 @@ struct Params {
   cudaGraphConditionalHandle cond;
 };
 
+// ---- optional per-tile timeline (profiling builds only: -DTSQ_TRACE) -------
+#ifdef TSQ_TRACE
+constexpr int kTraceTiles = 65536;
+__device__ u64 g_trace[kTraceTiles * 8];
+__device__ int g_trace_level;
+__device__ __forceinline__ void trace_mark(uint32_t level, uint32_t t, int slot) {
+  if ((int)level == g_trace_level && t < (uint32_t)kTraceTiles) {
+    u64 ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    g_trace[(size_t)t * 8 + slot] = ns;
+  }
+}
+#define TSQ_MARK(level, t, slot) trace_mark((level), (t), (slot))
+#else
+#define TSQ_MARK(level, t, slot) ((void)0)
+#endif
+
 // ---- order-preserving key codecs (native order -> unsigned order) ----------
 template <int DT> struct Codec;
 template <> struct Codec<TSQ_I32> {
@@ -200,6 +217,28 @@ __device__ __forceinline__ void mbar_wait(u64 *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// distinct copies per wait site so profiles attribute stalls to the role
+#define TSQ_WAIT_ASM                                                              \
+  "{\n\t.reg .pred p;\n\tTSQ_W_%=:\n\t"                                         \
+  "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t@!p bra TSQ_W_%=;\n\t}"
+__device__ __forceinline__ void wait_full_consumer(u64 *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void wait_full_counter(u64 *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void wait_ready_consumer(u64 *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void wait_empty_producer(u64 *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+}
+#undef TSQ_WAIT_ASM
+
 // 1-D bulk copy global -> shared, completing `bytes` on the mbarrier
 // (cp.async.bulk: SASS UBLKCP); dst/src 16-byte aligned, bytes % 16 == 0
 __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes,

@@ -37,23 +37,33 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
   typedef Geo<C, PAY> G;
   const int lane = threadIdx.x & 31;
   Ctl *ctl = P->ctl;
-  uint32_t t_next = 0;
-  if (lane == 0) t_next = atomicAdd(&ctl->tile_ticket, 1u);
+  const uint32_t level = ctl->level;
+  (void)level;
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
     const uint32_t j = it / kStages;
-    uint32_t t = __shfl_sync(0xffffffffu, t_next, 0);
+    // claim a tile only once a stage is free for it, so claim order tracks
+    // processing order across CTAs (the look-back waits on predecessors)
+    if (j > 0) wait_empty_producer(&empty[s], (j - 1) & 1u);
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(&ctl->tile_ticket, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
     StageMeta &m = meta[s];
     if (t >= ntiles) {
-      if (j > 0) mbar_wait(&empty[s], (j - 1) & 1u);
-      if (lane == 0) {
-        m.t = kDone;
-        mbar_arrive(&full[s]);
+      // end marker in this and the next kCounterWarps-1 stages: every
+      // counter warp (each owns every kCounterWarps-th fill) sees one
+      for (uint32_t e = 0; e < (uint32_t)kCounterWarps; ++e) {
+        const int se = (int)((it + e) % kStages);
+        const uint32_t je = (it + e) / kStages;
+        if (e > 0 && je > 0) wait_empty_producer(&empty[se], (je - 1) & 1u);
+        if (lane == 0) {
+          meta[se].t = kDone;
+          mbar_arrive(&full[se]);
+        }
       }
       return;
     }
-    // claim the following tile now; its atomic overlaps this tile's work
-    if (lane == 0) t_next = atomicAdd(&ctl->tile_ticket, 1u);
+    TSQ_MARK(level, t, 0);
     const uint32_t sid = P->tilemap[cur][t];
     const Seg *sgp = &P->segs[cur][sid];
     const long long begin = sgp->begin, end = sgp->end;
@@ -67,7 +77,6 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
     const uint32_t *psrc = PAY ? P->pay[buf] : nullptr;
     uint32_t skip = 0;
     if (kind != KIND_PARTITION) skip = ld_volatile32(&sgp->fail) != 0 ? 1u : 0u;
-    if (j > 0) mbar_wait(&empty[s], (j - 1) & 1u);
     U *dk = in_k + (size_t)s * G::TILE;
     uint32_t *dp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
     uint32_t tx = 0;
@@ -104,6 +113,7 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
         m.next_key = (u64)v;
         m.has_next = 1;
       }
+      TSQ_MARK(level, t, 1);
       if (tx) {
         mbar_arrive_expect_tx(&full[s], tx);
         bulk_load(dk + (a0 - tstart), src + a0, (uint32_t)((a1 - a0) * sizeof(U)), &full[s]);
@@ -121,25 +131,30 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
 template <class C, bool PAY>
 __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typename C::U *in_k,
                                              u64 *full, u64 *ready, u64 *empty,
-                                             StageMeta *meta) {
+                                             StageMeta *meta, int cw) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   const int lane = threadIdx.x & 31;
   u64 *lb = P->lookback[cur];
-  for (uint32_t it = 0;; ++it) {
+  const uint32_t level = P->ctl->level;
+  (void)level;
+  for (uint32_t it = cw;; it += kCounterWarps) {
     const int s = (int)(it % kStages);
-    mbar_wait(&full[s], (it / kStages) & 1u);
+    wait_full_counter(&full[s], (it / kStages) & 1u);
     StageMeta &m = meta[s];
     const uint32_t t = m.t;
+    if (t != kDone) TSQ_MARK(level, t, 2);
     if (t == kDone) return;
     if (m.kind == KIND_PARTITION) {
       const U piv = (U)m.pivot;
       const bool raw = P->raw[m.buf] != 0;
       const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
       const U *sk = in_k + (size_t)s * G::TILE;
-      uint32_t lt = 0, gt = 0;
+      uint32_t lta[G::VN], gta[G::VN];  // independent accumulators per lane slot
+#pragma unroll
+      for (int q = 0; q < G::VN; ++q) lta[q] = gta[q] = 0;
       const bool full_tile = rlo == 0 && rhi == G::TILE;
-#pragma unroll 4
+#pragma unroll 8
       for (int v = lane; v < G::TILE / G::VN; v += 32) {
         U kk[G::VN];
         unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + v * G::VN), kk);
@@ -148,9 +163,15 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
           const int idx = v * G::VN + q;
           const U x = raw ? C::enc(kk[q]) : kk[q];
           const bool ok = full_tile || (idx >= rlo && idx < rhi);
-          lt += (ok && x < piv) ? 1u : 0u;
-          gt += (ok && x > piv) ? 1u : 0u;
+          lta[q] += (ok && x < piv) ? 1u : 0u;
+          gta[q] += (ok && x > piv) ? 1u : 0u;
         }
+      }
+      uint32_t lt = 0, gt = 0;
+#pragma unroll
+      for (int q = 0; q < G::VN; ++q) {
+        lt += lta[q];
+        gt += gta[q];
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -161,8 +182,10 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       u64 excl = 0;
       if (m.k == 0) {
         if (lane == 0) st_volatile(&lb[t], kFlagInc | agg);
+        if (lane == 0) TSQ_MARK(level, t, 3);
       } else {
         if (lane == 0) st_volatile(&lb[t], kFlagAgg | agg);
+        if (lane == 0) TSQ_MARK(level, t, 3);
         long long base = (long long)t - 1;
         const long long stop = (long long)m.tile_base;
         for (;;) {
@@ -183,6 +206,7 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
           base -= 32;
         }
         if (lane == 0) st_volatile(&lb[t], kFlagInc | (excl + agg));
+        if (lane == 0) TSQ_MARK(level, t, 4);
       }
       if (lane == 0) m.excl = excl;
     }
@@ -231,6 +255,9 @@ __device__ __forceinline__ void consume_partition(const Params *P, const StageMe
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const StageMeta m = *mp;
+  const uint32_t level = P->ctl->level;
+  (void)level;
+  if (tid == 0) TSQ_MARK(level, m.t, 5);
   const int sb = (int)m.buf, db = sb ^ 1;
   const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
   const U piv = (U)m.pivot;
@@ -286,7 +313,8 @@ __device__ __forceinline__ void consume_partition(const Params *P, const StageMe
     t_lt += a; t_eq += b; t_gt += c;
   }
   // the tile's offsets from the counter warp; then the stage can be reused
-  mbar_wait(ready_s, ready_par);
+  wait_ready_consumer(ready_s, ready_par);
+  if (tid == 0) TSQ_MARK(level, m.t, 6);
   const u64 ex = mp->excl;
   const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
   const long long D_lt = m.begin + ex_lt;                  // first slot of this tile's < run
@@ -333,6 +361,7 @@ __device__ __forceinline__ void consume_partition(const Params *P, const StageMe
     emit_run<uint32_t>(P->side_pay, D_eq, t_eq, op + e_base, issuer, 5);
   }
   if (issuer) bulk_commit();
+  if (tid == 0) TSQ_MARK(level, m.t, 7);
 }
 
 // one verification tile: every adjacent pair inside the tile and the pair
@@ -373,7 +402,7 @@ __device__ __forceinline__ void consume_verify(const Params *P, int cur, const S
 }
 
 template <class C, bool PAY>
-__global__ void __launch_bounds__(kPartThreads, PAY ? 2 : 3)
+__global__ void __launch_bounds__(kPartThreads, 2)
     partition_kernel(const Params *__restrict__ P) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
@@ -406,14 +435,14 @@ __global__ void __launch_bounds__(kPartThreads, PAY ? 2 : 3)
     producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
     return;
   }
-  if (warp == kCounterWarp) {
-    counter_loop<C, PAY>(P, cur, in_k, full, ready, empty, meta);
+  if (warp >= kCounterWarp) {
+    counter_loop<C, PAY>(P, cur, in_k, full, ready, empty, meta, warp - kCounterWarp);
     return;
   }
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
     const uint32_t par = (it / kStages) & 1u;
-    mbar_wait(&full[s], par);
+    wait_full_consumer(&full[s], par);
     if (meta[s].t == kDone) break;
     const U *sk = in_k + (size_t)s * G::TILE;
     if (meta[s].kind == KIND_PARTITION) {
