@@ -225,7 +225,7 @@ __device__ __forceinline__ void wait_full_consumer(u64 *bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
 }
-__device__ __forceinline__ void wait_full_counter(u64 *bar, uint32_t parity) {
+__device__ __forceinline__ void wait_aggr_lookback(u64 *bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
 }

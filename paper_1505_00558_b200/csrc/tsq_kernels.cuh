@@ -37,9 +37,8 @@ namespace tsq {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;   // 256
 constexpr int kProducerWarp = kConsumerWarps;     // warp 8: tile claims + bulk loads
-constexpr int kCounterWarp = kConsumerWarps + 1;  // warps 9..: counts + look-back
-constexpr int kCounterWarps = 2;                  // alternate stages between them
-constexpr int kPartThreads = kConsumers + 32 * (1 + kCounterWarps);
+constexpr int kLookbackWarp = kConsumerWarps + 1; // warp 9: decoupled look-back
+constexpr int kPartThreads = kConsumers + 64;
 constexpr int kStages = 4;                        // input ring depth
 constexpr int kAlign = 4;                         // bulk-copy element alignment
 constexpr int kOutPad = 16;                       // alignment slack of the out buffer
@@ -70,11 +69,11 @@ __device__ __forceinline__ void unpack(const uint2 &v, uint32_t *o) {
 }
 
 // Tile descriptor handed from the producer warp to the counter and consumer
-// warps; `excl` (the tile's exclusive (<, >) prefix in its segment) is filled
-// in by the counter warp.
+// warps; `agg` (the tile's (<, >) counts) is filled in by the consumers and
+// `excl` (its exclusive prefix in its segment) by the look-back warp.
 struct StageMeta {
   long long tstart, lo, hi, begin, end;
-  u64 pivot, next_key, excl;
+  u64 pivot, next_key, agg, excl;
   uint32_t t, k, kind, buf, tile_base, sid, skip, has_next;
 };
 

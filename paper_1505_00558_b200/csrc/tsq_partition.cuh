@@ -7,21 +7,24 @@
 // block (retired, never compared again) in between (core.py:944-967).
 //
 // Persistent CTAs, warp-specialised (320 threads):
-//   warp 8  producer  claims tiles (one atomic ticket each, one claim ahead),
-//                     resolves their segment, and streams the tile into a
-//                     3-deep shared-memory ring with cp.async.bulk (TMA
-//                     engine) completing on the stage's mbarrier
-//   warp 9  counter   as soon as a stage lands: counts its < / > keys,
-//                     publishes the tile aggregate, resolves the tile's
-//                     exclusive prefix by decoupled look-back over the
-//                     segment's earlier tiles, publishes the inclusive
-//                     prefix and hands the offset to the consumers
-//   warps 0-7 consumers  classify every key against the pivot, rank it in
-//                     its class with __ballot_sync / __popc, stage the < run
-//                     and the > run (and, for records, the == payloads) in
-//                     shared memory aligned like their destinations, and
-//                     write them with cp.async.bulk stores (scalar stores for
-//                     the <= 3 unaligned keys at each end)
+//   warp 8  producer   claims a tile (one atomic ticket) as soon as a stage of
+//                      the 4-deep shared-memory ring is free, resolves its
+//                      segment, and streams it in with cp.async.bulk (TMA
+//                      engine) completing on the stage's mbarrier
+//   warp 9  look-back  for each stage in order: once the consumers published
+//                      the tile's (<, >) aggregate, resolves the tile's
+//                      exclusive prefix in its segment by decoupled look-back
+//                      over the segment's earlier tiles and publishes the
+//                      inclusive prefix
+//   warps 0-7 consumers  software-pipelined by one tile: classify tile k+1
+//                      (every key against the pivot, ranked in its class with
+//                      __ballot_sync / __popc) and publish its aggregate,
+//                      then stage tile k's < run and > run (and, for records,
+//                      its == payloads) in shared memory aligned like their
+//                      destinations and write them with cp.async.bulk stores
+//                      (scalar stores for the <= 3 unaligned keys at each end)
+// The one-tile skew gives every look-back a full tile of consumer work to
+// complete in, so the consumers rarely wait for offsets.
 #pragma once
 
 namespace tsq {
@@ -50,16 +53,9 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
     t = __shfl_sync(0xffffffffu, t, 0);
     StageMeta &m = meta[s];
     if (t >= ntiles) {
-      // end marker in this and the next kCounterWarps-1 stages: every
-      // counter warp (each owns every kCounterWarps-th fill) sees one
-      for (uint32_t e = 0; e < (uint32_t)kCounterWarps; ++e) {
-        const int se = (int)((it + e) % kStages);
-        const uint32_t je = (it + e) / kStages;
-        if (e > 0 && je > 0) wait_empty_producer(&empty[se], (je - 1) & 1u);
-        if (lane == 0) {
-          meta[se].t = kDone;
-          mbar_arrive(&full[se]);
-        }
+      if (lane == 0) {
+        m.t = kDone;
+        mbar_arrive(&full[s]);
       }
       return;
     }
@@ -126,95 +122,52 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// Counter warp: tile aggregate + decoupled look-back, ahead of the consumers.
+// Look-back warp.
 
-template <class C, bool PAY>
-__device__ __forceinline__ void counter_loop(const Params *P, int cur, const typename C::U *in_k,
-                                             u64 *full, u64 *ready, u64 *empty,
-                                             StageMeta *meta, int cw) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
+__device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
+                                              StageMeta *meta) {
   const int lane = threadIdx.x & 31;
   u64 *lb = P->lookback[cur];
   const uint32_t level = P->ctl->level;
   (void)level;
-  for (uint32_t it = cw;; it += kCounterWarps) {
+  for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
-    wait_full_counter(&full[s], (it / kStages) & 1u);
+    wait_aggr_lookback(&aggr[s], (it / kStages) & 1u);
     StageMeta &m = meta[s];
     const uint32_t t = m.t;
-    if (t != kDone) TSQ_MARK(level, t, 2);
     if (t == kDone) return;
-    if (m.kind == KIND_PARTITION) {
-      const U piv = (U)m.pivot;
-      const bool raw = P->raw[m.buf] != 0;
-      const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
-      const U *sk = in_k + (size_t)s * G::TILE;
-      uint32_t lta[G::VN], gta[G::VN];  // independent accumulators per lane slot
-#pragma unroll
-      for (int q = 0; q < G::VN; ++q) lta[q] = gta[q] = 0;
-      const bool full_tile = rlo == 0 && rhi == G::TILE;
-#pragma unroll 8
-      for (int v = lane; v < G::TILE / G::VN; v += 32) {
-        U kk[G::VN];
-        unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + v * G::VN), kk);
-#pragma unroll
-        for (int q = 0; q < G::VN; ++q) {
-          const int idx = v * G::VN + q;
-          const U x = raw ? C::enc(kk[q]) : kk[q];
-          const bool ok = full_tile || (idx >= rlo && idx < rhi);
-          lta[q] += (ok && x < piv) ? 1u : 0u;
-          gta[q] += (ok && x > piv) ? 1u : 0u;
-        }
-      }
-      uint32_t lt = 0, gt = 0;
-#pragma unroll
-      for (int q = 0; q < G::VN; ++q) {
-        lt += lta[q];
-        gt += gta[q];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lt += __shfl_xor_sync(0xffffffffu, lt, o);
-        gt += __shfl_xor_sync(0xffffffffu, gt, o);
-      }
-      const u64 agg = ((u64)lt << 31) | (u64)gt;
+    if (m.kind == KIND_PARTITION && m.k > 0) {
+      const u64 agg = m.agg;
       u64 excl = 0;
-      if (m.k == 0) {
-        if (lane == 0) st_volatile(&lb[t], kFlagInc | agg);
-        if (lane == 0) TSQ_MARK(level, t, 3);
-      } else {
-        if (lane == 0) st_volatile(&lb[t], kFlagAgg | agg);
-        if (lane == 0) TSQ_MARK(level, t, 3);
-        long long base = (long long)t - 1;
-        const long long stop = (long long)m.tile_base;
-        for (;;) {
-          const long long idx = base - lane;
-          u64 d = kFlagInc;
-          if (idx >= stop) {
-            do {
-              d = ld_volatile(&lb[idx]);
-            } while ((d >> 62) == 0);
-          }
-          const uint32_t inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
-          if (inc) {
-            const int first = __ffs(inc) - 1;
-            excl += warp_sum64(lane <= first ? (d & kValMask) : 0ull);
-            break;
-          }
-          excl += warp_sum64(d & kValMask);
-          base -= 32;
+      long long base = (long long)t - 1;
+      const long long stop = (long long)m.tile_base;
+      for (;;) {
+        const long long idx = base - lane;
+        u64 d = kFlagInc;
+        if (idx >= stop) {
+          do {
+            d = ld_volatile(&lb[idx]);
+          } while ((d >> 62) == 0);
         }
-        if (lane == 0) st_volatile(&lb[t], kFlagInc | (excl + agg));
-        if (lane == 0) TSQ_MARK(level, t, 4);
+        const uint32_t inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+        if (inc) {
+          const int first = __ffs(inc) - 1;
+          excl += warp_sum64(lane <= first ? (d & kValMask) : 0ull);
+          break;
+        }
+        excl += warp_sum64(d & kValMask);
+        base -= 32;
       }
-      if (lane == 0) m.excl = excl;
+      if (lane == 0) {
+        st_volatile(&lb[t], kFlagInc | (excl + agg));
+        TSQ_MARK(level, t, 4);
+        m.excl = excl;
+      }
+    } else if (lane == 0) {
+      m.excl = 0;
     }
     __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&ready[s]);
-      mbar_arrive(&empty[s]);
-    }
+    if (lane == 0) mbar_arrive(&ready[s]);
   }
 }
 
@@ -223,7 +176,7 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
 
 // Write one staged run: element j of the run (global index D + j) sits at
 // R[(D & 3) + j]; the 16B-aligned body goes out as one bulk store issued by
-// `issuer`, the <= 3 keys at each ragged end as scalar stores by `lane` < 8
+// `issuer`, the <= 3 keys at each ragged end as scalar stores by lanes < 8
 // of warp `scal_warp`.
 template <typename T>
 __device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T *R,
@@ -237,140 +190,29 @@ __device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T
     bulk_store(g + b0, R + (b0 - base), (uint32_t)((b1 - b0) * (long long)sizeof(T)));
   if ((int)(threadIdx.x >> 5) == scal_warp) {
     const int lane = threadIdx.x & 31;
-    const long long h = body ? (b0 - D) : L;            // head count (all if no body)
-    const long long ts = body ? (b1 - D) : L;           // tail start
+    const long long h = body ? (b0 - D) : L;   // head count (all if no body)
+    const long long ts = body ? (b1 - D) : L;  // tail start
     const long long e = lane < h ? lane : ts + (lane - h);
     if (lane < 8 && (lane < h || e < L)) g[D + e] = R[(D - base) + e];
   }
 }
 
-template <class C, bool PAY>
-__device__ __forceinline__ void consume_partition(const Params *P, const StageMeta *mp,
-                                                  const typename C::U *sk, const uint32_t *sp,
-                                                  u64 *ready_s, uint32_t ready_par,
-                                                  u64 *empty_s, typename C::U *ok,
-                                                  uint32_t *op, uint32_t (*wcnt)[3]) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const StageMeta m = *mp;
-  const uint32_t level = P->ctl->level;
-  (void)level;
-  if (tid == 0) TSQ_MARK(level, m.t, 5);
-  const int sb = (int)m.buf, db = sb ^ 1;
-  const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
-  const U piv = (U)m.pivot;
-  const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
-  const bool full_tile = rlo == 0 && rhi == G::TILE;
-
-  // keys stay in the shared-memory stage until they are staged for output;
-  // registers carry only (class << 16 | rank) per key
-  uint32_t cls[G::IPT];  // class (0 <, 1 ==, 2 >, 3 none) << 16 | rank in class
-#pragma unroll
-  for (int v = 0; v < G::VPT; ++v) {
-    const int e0 = (v * kConsumers + tid) * G::VN;
-    U key[G::VN];
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
-#pragma unroll
-    for (int q = 0; q < G::VN; ++q) {
-      const int idx = e0 + q;
-      const U x = src_raw ? C::enc(key[q]) : key[q];
-      cls[v * G::VN + q] = (full_tile || (idx >= rlo && idx < rhi))
-                               ? (x < piv ? 0u : (x == piv ? 1u : 2u))
-                               : 3u;
-    }
-  }
-  // warp-level ranks per class, ordered by (item, lane)
-  const uint32_t lmask = (1u << lane) - 1u;
-  uint32_t lt_run = 0, gt_run = 0, eq_run = 0;
-#pragma unroll
-  for (int i = 0; i < G::IPT; ++i) {
-    const uint32_t blt = __ballot_sync(0xffffffffu, cls[i] == 0);
-    const uint32_t bgt = __ballot_sync(0xffffffffu, cls[i] == 2);
-    const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, cls[i] == 1) : 0u;
-    const uint32_t bm = cls[i] == 0 ? blt : (cls[i] == 2 ? bgt : beq);
-    const uint32_t base = cls[i] == 0 ? lt_run : (cls[i] == 2 ? gt_run : eq_run);
-    cls[i] = (cls[i] << 16) | (base + __popc(bm & lmask));
-    lt_run += __popc(blt);
-    gt_run += __popc(bgt);
-    eq_run += __popc(beq);
-  }
-  if (lane == 0) {
-    wcnt[warp][0] = lt_run;
-    wcnt[warp][1] = eq_run;
-    wcnt[warp][2] = gt_run;
-  }
-  // the previous tile's bulk stores must have finished reading the out
-  // buffer before it is restaged
-  if (tid == 0) bulk_wait_read0();
-  named_sync(1, kConsumers);
-  uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
-#pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) {
-    const uint32_t a = wcnt[w][0], b = wcnt[w][1], c = wcnt[w][2];
-    if (w < warp) { w_lt += a; w_eq += b; w_gt += c; }
-    t_lt += a; t_eq += b; t_gt += c;
-  }
-  // the tile's offsets from the counter warp; then the stage can be reused
-  wait_ready_consumer(ready_s, ready_par);
-  if (tid == 0) TSQ_MARK(level, m.t, 6);
-  const u64 ex = mp->excl;
-  const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
-  const long long D_lt = m.begin + ex_lt;                  // first slot of this tile's < run
-  const long long D_gt = m.end - ex_gt - (long long)t_gt;  // first slot of its > run
-  const long long ex_eq = (m.lo - m.begin) - ex_lt - ex_gt;
-  const long long D_eq = m.begin + ex_eq;                  // records: side buffer slot
-  const int o_lt = (int)(D_lt & (kAlign - 1));
-  const int g_base = (o_lt + (int)t_lt + kAlign - 1) & ~(kAlign - 1);
-  const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
-  const int e_base = (o_gt + (int)t_gt + kAlign - 1) & ~(kAlign - 1);
-  const int o_eq = e_base + (int)(D_eq & (kAlign - 1));
-#pragma unroll
-  for (int i = 0; i < G::IPT; ++i) {
-    const uint32_t c = cls[i] >> 16, rk = cls[i] & 0xffffu;
-    if (c == 3u) continue;
-    int pos;
-    if (c == 0u) pos = o_lt + (int)(w_lt + rk);
-    else if (c == 2u) pos = o_gt + (int)(t_gt - 1u - (w_gt + rk));  // > run fills backwards
-    else {
-      if (!PAY) continue;
-      pos = o_eq + (int)(w_eq + rk);
-    }
-    const int e = ((i / G::VN) * kConsumers + tid) * G::VN + (i % G::VN);
-    if (c != 1u) {
-      U x = sk[e];
-      if (src_raw != dst_raw) x = src_raw ? C::enc(x) : C::dec(x);
-      ok[pos] = x;
-    }
-    if (PAY) op[pos] = sp[e];
-  }
-  // the stage is no longer needed: hand it back to the producer
-  __syncwarp();
-  if (lane == 0) mbar_arrive(empty_s);
-  fence_proxy_async_smem();
-  named_sync(1, kConsumers);
-  U *dst = reinterpret_cast<U *>(P->keys[db]);
-  const bool issuer = tid == 0;
-  emit_run<U>(dst, D_lt, t_lt, ok, issuer, 1);
-  emit_run<U>(dst, D_gt, t_gt, ok + g_base, issuer, 2);
-  if (PAY) {
-    uint32_t *dpay = P->pay[db];
-    emit_run<uint32_t>(dpay, D_lt, t_lt, op, issuer, 3);
-    emit_run<uint32_t>(dpay, D_gt, t_gt, op + g_base, issuer, 4);
-    emit_run<uint32_t>(P->side_pay, D_eq, t_eq, op + e_base, issuer, 5);
-  }
-  if (issuer) bulk_commit();
-  if (tid == 0) TSQ_MARK(level, m.t, 7);
-}
+// What the consumers carry from classifying a tile to emitting it.
+template <int IPT>
+struct TileState {
+  int s;
+  uint32_t par;
+  uint32_t partition;  // 0 for a verification tile
+  uint32_t t_lt, t_gt, t_eq, w_lt, w_gt, w_eq;
+  uint32_t cls[IPT];   // class (0 <, 1 ==, 2 >, 3 none) << 16 | rank in class
+};
 
 // one verification tile: every adjacent pair inside the tile and the pair
 // that crosses into the next tile must be ordered; a violation marks the
 // segment failed (its later tiles are skipped by the producer)
 template <class C, bool PAY>
-__device__ __forceinline__ void consume_verify(const Params *P, int cur, const StageMeta &m,
-                                               const typename C::U *sk, u64 *empty_s,
-                                               uint32_t *s_flag) {
+__device__ __forceinline__ void verify_tile(const Params *P, int cur, const StageMeta &m,
+                                            const typename C::U *sk, uint32_t *s_flag) {
   typedef typename C::U U;
   const int tid = threadIdx.x;
   const bool raw = P->raw[m.buf] != 0;
@@ -395,15 +237,190 @@ __device__ __forceinline__ void consume_verify(const Params *P, int cur, const S
   if (tid == 0) *s_flag = 0;
   named_sync(1, kConsumers);
   if (bad) *s_flag = 1;
-  __syncwarp();
-  if ((tid & 31) == 0) mbar_arrive(empty_s);
   named_sync(1, kConsumers);
   if (tid == 0 && *s_flag) atomicOr(&P->segs[cur][m.sid].fail, 1u);
 }
 
+// Phase A of tile `it`: classify and rank every key, publish the aggregate.
+// Returns false at the end-of-level marker.
 template <class C, bool PAY>
-__global__ void __launch_bounds__(kPartThreads, 2)
-    partition_kernel(const Params *__restrict__ P) {
+__device__ __forceinline__ bool classify_tile(const Params *P, int cur, uint32_t it,
+                                              const typename C::U *in_k, u64 *full, u64 *aggr,
+                                              StageMeta *meta, uint32_t (*wcnt)[3],
+                                              uint32_t *s_flag, TileState<Geo<C, PAY>::IPT> &ts) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  ts.s = (int)(it % kStages);
+  ts.par = (it / kStages) & 1u;
+  wait_full_consumer(&full[ts.s], ts.par);
+  const StageMeta &m = meta[ts.s];
+  const uint32_t t = m.t;
+  if (t == kDone) {
+    if (tid == 0) mbar_arrive(&aggr[ts.s]);  // lets the look-back warp see the end
+    return false;
+  }
+  const U *sk = in_k + (size_t)ts.s * G::TILE;
+  const uint32_t level = P->ctl->level;
+  (void)level;
+  if (tid == 0) TSQ_MARK(level, t, 2);
+  if (m.kind != KIND_PARTITION) {
+    ts.partition = 0;
+    verify_tile<C, PAY>(P, cur, m, sk, s_flag);
+    if (tid == 0) mbar_arrive(&aggr[ts.s]);
+    return true;
+  }
+  ts.partition = 1;
+  const bool src_raw = P->raw[m.buf] != 0;
+  const U piv = (U)m.pivot;
+  const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
+  const bool full_tile = rlo == 0 && rhi == G::TILE;
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + tid) * G::VN;
+    U key[G::VN];
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) {
+      const int idx = e0 + q;
+      const U x = src_raw ? C::enc(key[q]) : key[q];
+      ts.cls[v * G::VN + q] = (full_tile || (idx >= rlo && idx < rhi))
+                                  ? (x < piv ? 0u : (x == piv ? 1u : 2u))
+                                  : 3u;
+    }
+  }
+  // warp-level ranks per class, ordered by (item, lane)
+  const uint32_t lmask = (1u << lane) - 1u;
+  uint32_t lt_run = 0, gt_run = 0, eq_run = 0;
+#pragma unroll
+  for (int i = 0; i < G::IPT; ++i) {
+    const uint32_t c = ts.cls[i];
+    const uint32_t blt = __ballot_sync(0xffffffffu, c == 0);
+    const uint32_t bgt = __ballot_sync(0xffffffffu, c == 2);
+    const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, c == 1) : 0u;
+    const uint32_t bm = c == 0 ? blt : (c == 2 ? bgt : beq);
+    const uint32_t base = c == 0 ? lt_run : (c == 2 ? gt_run : eq_run);
+    ts.cls[i] = (c << 16) | (base + __popc(bm & lmask));
+    lt_run += __popc(blt);
+    gt_run += __popc(bgt);
+    if (PAY) eq_run += __popc(beq);
+  }
+  uint32_t(*wc)[3] = wcnt + (it & 1u) * kConsumerWarps;
+  if (lane == 0) {
+    wc[warp][0] = lt_run;
+    wc[warp][1] = eq_run;
+    wc[warp][2] = gt_run;
+  }
+  // the previous tile's bulk stores must have finished reading the out
+  // buffer before the tile after this barrier restages it
+  if (tid == 0) bulk_wait_read0();
+  named_sync(1, kConsumers);
+  uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) {
+    const uint32_t a = wc[w][0], b = wc[w][1], c = wc[w][2];
+    if (w < warp) { w_lt += a; w_eq += b; w_gt += c; }
+    t_lt += a; t_eq += b; t_gt += c;
+  }
+  ts.w_lt = w_lt; ts.w_eq = w_eq; ts.w_gt = w_gt;
+  ts.t_lt = t_lt; ts.t_eq = t_eq; ts.t_gt = t_gt;
+  if (tid == 0) {
+    const u64 agg = ((u64)t_lt << 31) | (u64)t_gt;
+    StageMeta &mw = meta[ts.s];
+    mw.agg = agg;
+    st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
+    TSQ_MARK(level, t, 3);
+    mbar_arrive(&aggr[ts.s]);
+  }
+  return true;
+}
+
+// Phase B of a tile: wait for its offsets, stage its runs, write them out.
+template <class C, bool PAY>
+__device__ __forceinline__ void emit_tile(const Params *P, const typename C::U *in_k,
+                                          const uint32_t *in_p, u64 *ready, u64 *empty,
+                                          StageMeta *meta, typename C::U *ok, uint32_t *op,
+                                          const TileState<Geo<C, PAY>::IPT> &ts) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (!ts.partition) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[ts.s]);
+    return;
+  }
+  const StageMeta &m = meta[ts.s];
+  const uint32_t level = P->ctl->level;
+  (void)level;
+  if (tid == 0) TSQ_MARK(level, m.t, 5);
+  wait_ready_consumer(&ready[ts.s], ts.par);
+  if (tid == 0) TSQ_MARK(level, m.t, 6);
+  const u64 ex = m.excl;
+  const int sb = (int)m.buf, db = sb ^ 1;
+  const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
+  const long long begin = m.begin, end = m.end, lo = m.lo;
+  const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
+  const long long D_lt = begin + ex_lt;                      // first slot of this tile's < run
+  const long long D_gt = end - ex_gt - (long long)ts.t_gt;   // first slot of its > run
+  const long long D_eq = begin + (lo - begin) - ex_lt - ex_gt;  // records: side-buffer slot
+  const int o_lt = (int)(D_lt & (kAlign - 1));
+  const int g_base = (o_lt + (int)ts.t_lt + kAlign - 1) & ~(kAlign - 1);
+  const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
+  const int e_base = (o_gt + (int)ts.t_gt + kAlign - 1) & ~(kAlign - 1);
+  const int o_eq = e_base + (int)(D_eq & (kAlign - 1));
+  const U *sk = in_k + (size_t)ts.s * G::TILE;
+  const uint32_t *sp = PAY ? in_p + (size_t)ts.s * G::TILE : nullptr;
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + tid) * G::VN;
+    U key[G::VN];
+    uint32_t pay[G::VN];
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay);
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) {
+      const uint32_t cr = ts.cls[v * G::VN + q];
+      const uint32_t c = cr >> 16, rk = cr & 0xffffu;
+      if (c == 3u || (!PAY && c == 1u)) continue;
+      int pos;
+      if (c == 0u) pos = o_lt + (int)(ts.w_lt + rk);
+      else if (c == 2u) pos = o_gt + (int)(ts.t_gt - 1u - (ts.w_gt + rk));  // > run fills backwards
+      else pos = o_eq + (int)(ts.w_eq + rk);
+      if (c != 1u) {
+        U x = key[q];
+        if (src_raw != dst_raw) x = src_raw ? C::enc(x) : C::dec(x);
+        ok[pos] = x;
+      }
+      if (PAY) op[pos] = pay[q];
+    }
+  }
+  const uint32_t t = m.t;
+  (void)t;
+  // the stage is no longer needed: hand it back to the producer
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&empty[ts.s]);
+  fence_proxy_async_smem();
+  named_sync(1, kConsumers);
+  U *dst = reinterpret_cast<U *>(P->keys[db]);
+  const bool issuer = tid == 0;
+  emit_run<U>(dst, D_lt, ts.t_lt, ok, issuer, 1);
+  emit_run<U>(dst, D_gt, ts.t_gt, ok + g_base, issuer, 2);
+  if (PAY) {
+    uint32_t *dpay = P->pay[db];
+    emit_run<uint32_t>(dpay, D_lt, ts.t_lt, op, issuer, 3);
+    emit_run<uint32_t>(dpay, D_gt, ts.t_gt, op + g_base, issuer, 4);
+    emit_run<uint32_t>(P->side_pay, D_eq, ts.t_eq, op + e_base, issuer, 5);
+  }
+  if (issuer) {
+    bulk_commit();
+    TSQ_MARK(level, t, 7);
+  }
+}
+
+template <class C, bool PAY>
+__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ P) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -412,9 +429,9 @@ __global__ void __launch_bounds__(kPartThreads, 2)
   U *out_k = reinterpret_cast<U *>(smem_raw + (size_t)kStages * G::STAGE_BYTES);
   uint32_t *out_p = reinterpret_cast<uint32_t *>(smem_raw + (size_t)kStages * G::STAGE_BYTES +
                                                  G::OUT_K);
-  __shared__ __align__(8) u64 full[kStages], ready[kStages], empty[kStages];
+  __shared__ __align__(8) u64 full[kStages], aggr[kStages], ready[kStages], empty[kStages];
   __shared__ StageMeta meta[kStages];
-  __shared__ uint32_t wcnt[kConsumerWarps][3];
+  __shared__ uint32_t wcnt[2 * kConsumerWarps][3];
   __shared__ uint32_t s_flag;
 
   Ctl *ctl = P->ctl;
@@ -424,8 +441,9 @@ __global__ void __launch_bounds__(kPartThreads, 2)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&aggr[s], 1);
       mbar_init(&ready[s], 1);
-      mbar_init(&empty[s], kConsumerWarps + 1);
+      mbar_init(&empty[s], kConsumerWarps);
     }
     fence_barrier_init();
   }
@@ -435,23 +453,19 @@ __global__ void __launch_bounds__(kPartThreads, 2)
     producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
     return;
   }
-  if (warp >= kCounterWarp) {
-    counter_loop<C, PAY>(P, cur, in_k, full, ready, empty, meta, warp - kCounterWarp);
+  if (warp == kLookbackWarp) {
+    lookback_loop(P, cur, aggr, ready, meta);
     return;
   }
-  for (uint32_t it = 0;; ++it) {
-    const int s = (int)(it % kStages);
-    const uint32_t par = (it / kStages) & 1u;
-    wait_full_consumer(&full[s], par);
-    if (meta[s].t == kDone) break;
-    const U *sk = in_k + (size_t)s * G::TILE;
-    if (meta[s].kind == KIND_PARTITION) {
-      consume_partition<C, PAY>(P, &meta[s], sk, in_p + (size_t)s * G::TILE, &ready[s], par,
-                                &empty[s], out_k, out_p, wcnt);
-    } else {
-      const StageMeta m = meta[s];
-      consume_verify<C, PAY>(P, cur, m, sk, &empty[s], &s_flag);
-    }
+  TileState<G::IPT> a, b;
+  bool more = classify_tile<C, PAY>(P, cur, 0, in_k, full, aggr, meta, wcnt, &s_flag, a);
+  for (uint32_t it = 1; more; ++it) {
+    // classify the next tile before emitting this one: its aggregate is
+    // published while this tile's look-back completes
+    const bool next = classify_tile<C, PAY>(P, cur, it, in_k, full, aggr, meta, wcnt, &s_flag, b);
+    emit_tile<C, PAY>(P, in_k, in_p, ready, empty, meta, out_k, out_p, a);
+    if (!next) break;
+    a = b;
   }
   if (threadIdx.x == 0) bulk_wait0();
 }

@@ -1,8 +1,8 @@
 """Per-tile timeline of one partition level (profiling build, dev tool).
 
     TSQ_LIB=paper_1505_00558_b200/libtsq_b200_trace.so python scripts/trace_level.py [level]
-Slots: 0 claim, 1 bulk load issued, 2 landed (counter), 3 aggregate
-published, 4 inclusive published, 5 consumer start, 6 offsets ready,
+Slots: 0 claim, 1 bulk load issued, 2 classify start, 3 aggregate
+published, 4 inclusive published (look-back warp), 5 emit start, 6 offsets ready,
 7 consumer emitted.
 """
 import ctypes
@@ -40,9 +40,9 @@ tr = tr.reshape(-1, 8)[:nt].astype(np.int64)
 t0 = tr[tr[:, 0] > 0, 0].min()
 tr = np.where(tr > 0, tr - t0, -1)
 print(f"level {level}: {lv}  tiles traced {nt}")
-names = ["resolve(1-0)", "load(2-1)", "count(3-2)", "lookback(4-3)", "cons_lag(5-2)",
+names = ["resolve(1-0)", "land+lag(2-1)", "classify(3-2)", "lookback(4-3)", "skew(5-3)",
          "ready_wait(6-5)", "stage+emit(7-6)", "total(7-0)"]
-pairs = [(1, 0), (2, 1), (3, 2), (4, 3), (5, 2), (6, 5), (7, 6), (7, 0)]
+pairs = [(1, 0), (2, 1), (3, 2), (4, 3), (5, 3), (6, 5), (7, 6), (7, 0)]
 for name, (a, b) in zip(names, pairs):
     ok = (tr[:, a] >= 0) & (tr[:, b] >= 0)
     x = (tr[ok, a] - tr[ok, b]) / 1000.0
