@@ -257,8 +257,15 @@ __device__ __forceinline__ bool classify_tile(const Params *P, int cur, uint32_t
   wait_full_consumer(&full[ts.s], ts.par);
   const StageMeta &m = meta[ts.s];
   const uint32_t t = m.t;
+  // Every path through here ends with a consumer barrier that thread 0
+  // (the bulk-store issuer) reaches only after the previous tile's bulk
+  // stores finished reading the out buffer, which the next emit restages.
   if (t == kDone) {
-    if (tid == 0) mbar_arrive(&aggr[ts.s]);  // lets the look-back warp see the end
+    if (tid == 0) {
+      mbar_arrive(&aggr[ts.s]);  // lets the look-back warp see the end
+      bulk_wait_read0();
+    }
+    named_sync(1, kConsumers);
     return false;
   }
   const U *sk = in_k + (size_t)ts.s * G::TILE;
@@ -267,6 +274,7 @@ __device__ __forceinline__ bool classify_tile(const Params *P, int cur, uint32_t
   if (tid == 0) TSQ_MARK(level, t, 2);
   if (m.kind != KIND_PARTITION) {
     ts.partition = 0;
+    if (tid == 0) bulk_wait_read0();
     verify_tile<C, PAY>(P, cur, m, sk, s_flag);
     if (tid == 0) mbar_arrive(&aggr[ts.s]);
     return true;
@@ -347,6 +355,9 @@ __device__ __forceinline__ void emit_tile(const Params *P, const typename C::U *
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   if (!ts.partition) {
+    // the look-back warp still walks this stage's meta: wait for it (this
+    // also keeps the aggr / ready phases of a stage from running ahead)
+    wait_ready_consumer(&ready[ts.s], ts.par);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ts.s]);
     return;

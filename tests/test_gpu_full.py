@@ -51,7 +51,7 @@ def test_full_size_family(cuda_ok, family):
         st = s.sort_with_stats(T.Records(dk, dp))
         assert W.sha16(dk.cpu().numpy()) == SORTED_SHA[family]
         # payload is a permutation of 0..n-1 whose keys agree position-wise
-        assert torch.equal(kin[dp.long()], dk)
+        assert torch.equal(kin.view(torch.int64)[dp.long()], dk.view(torch.int64))
         seen = torch.zeros(n, dtype=torch.int32, device="cuda")
         seen.index_add_(0, dp.long(), torch.ones(n, dtype=torch.int32, device="cuda"))
         assert bool((seen == 1).all())
