@@ -293,12 +293,14 @@ __device__ __forceinline__ bool classify_tile(const Params *P, int cur, uint32_t
     for (int q = 0; q < G::VN; ++q) {
       const int idx = e0 + q;
       const U x = src_raw ? C::enc(key[q]) : key[q];
-      ts.cls[v * G::VN + q] = (full_tile || (idx >= rlo && idx < rhi))
-                                  ? (x < piv ? 0u : (x == piv ? 1u : 2u))
-                                  : 3u;
+      const uint32_t valid = (full_tile || (idx >= rlo && idx < rhi)) ? 1u : 0u;
+      // 0 <, 1 ==, 2 >, 3 outside the segment (branch-free)
+      const uint32_t c = ((uint32_t)(x >= piv) + (uint32_t)(x > piv)) | ((valid ^ 1u) * 3u);
+      ts.cls[v * G::VN + q] = c;
     }
   }
-  // warp-level ranks per class, ordered by (item, lane)
+  // warp-level ranks per class, ordered by (item, lane); masks select the
+  // class's ballot and running count without branches
   const uint32_t lmask = (1u << lane) - 1u;
   uint32_t lt_run = 0, gt_run = 0, eq_run = 0;
 #pragma unroll
@@ -307,8 +309,10 @@ __device__ __forceinline__ bool classify_tile(const Params *P, int cur, uint32_t
     const uint32_t blt = __ballot_sync(0xffffffffu, c == 0);
     const uint32_t bgt = __ballot_sync(0xffffffffu, c == 2);
     const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, c == 1) : 0u;
-    const uint32_t bm = c == 0 ? blt : (c == 2 ? bgt : beq);
-    const uint32_t base = c == 0 ? lt_run : (c == 2 ? gt_run : eq_run);
+    const uint32_t mlt = 0u - (uint32_t)(c == 0), mgt = 0u - (uint32_t)(c == 2);
+    const uint32_t meq = PAY ? 0u - (uint32_t)(c == 1) : 0u;
+    const uint32_t bm = (blt & mlt) | (bgt & mgt) | (beq & meq);
+    const uint32_t base = (lt_run & mlt) | (gt_run & mgt) | (eq_run & meq);
     ts.cls[i] = (c << 16) | (base + __popc(bm & lmask));
     lt_run += __popc(blt);
     gt_run += __popc(bgt);
@@ -383,6 +387,9 @@ __device__ __forceinline__ void emit_tile(const Params *P, const typename C::U *
   const int o_eq = e_base + (int)(D_eq & (kAlign - 1));
   const U *sk = in_k + (size_t)ts.s * G::TILE;
   const uint32_t *sp = PAY ? in_p + (size_t)ts.s * G::TILE : nullptr;
+  const uint32_t lt0 = (uint32_t)o_lt + ts.w_lt;
+  const uint32_t gt0 = (uint32_t)o_gt + ts.t_gt - 1u - ts.w_gt;
+  const uint32_t eq0 = (uint32_t)o_eq + ts.w_eq;
 #pragma unroll
   for (int v = 0; v < G::VPT; ++v) {
     const int e0 = (v * kConsumers + tid) * G::VN;
@@ -392,19 +399,17 @@ __device__ __forceinline__ void emit_tile(const Params *P, const typename C::U *
     if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay);
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) {
+      // branch-free: select the slot, predicate the stores
       const uint32_t cr = ts.cls[v * G::VN + q];
       const uint32_t c = cr >> 16, rk = cr & 0xffffu;
-      if (c == 3u || (!PAY && c == 1u)) continue;
-      int pos;
-      if (c == 0u) pos = o_lt + (int)(ts.w_lt + rk);
-      else if (c == 2u) pos = o_gt + (int)(ts.t_gt - 1u - (ts.w_gt + rk));  // > run fills backwards
-      else pos = o_eq + (int)(ts.w_eq + rk);
-      if (c != 1u) {
-        U x = key[q];
-        if (src_raw != dst_raw) x = src_raw ? C::enc(x) : C::dec(x);
-        ok[pos] = x;
-      }
-      if (PAY) op[pos] = pay[q];
+      const uint32_t p_lt = lt0 + rk;
+      const uint32_t p_gt = gt0 - rk;  // > run fills backwards
+      uint32_t pos = c == 0u ? p_lt : p_gt;
+      if (PAY) pos = c == 1u ? eq0 + rk : pos;
+      U x = key[q];
+      if (src_raw != dst_raw) x = src_raw ? C::enc(x) : C::dec(x);
+      if ((c & 1u) == 0u) ok[pos] = x;   // c == 0 or c == 2
+      if (PAY && c != 3u) op[pos] = pay[q];
     }
   }
   const uint32_t t = m.t;
