@@ -124,6 +124,51 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
 // ---------------------------------------------------------------------------
 // Look-back warp.
 
+// Decoupled look-back of one tile: the exclusive (<, >) prefix of tile
+// `base + 1` over the tiles [stop, base] of its segment.  Each round trip
+// reads a window of 32 * kLbPerLane descriptors (lane l holds distances
+// l*kLbPerLane .. l*kLbPerLane + kLbPerLane - 1, nearest first), stops at
+// the nearest inclusive prefix and only re-reads when a descriptor nearer
+// than that one is not yet published; tiles before `stop` count as an
+// inclusive zero (segment start).
+constexpr int kLbPerLane = 8;
+
+__device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long long stop) {
+  const int lane = threadIdx.x & 31;
+  u64 excl = 0;
+  for (;;) {
+    u64 d[kLbPerLane];
+#pragma unroll
+    for (int e = 0; e < kLbPerLane; ++e) {
+      const long long idx = base - (lane * kLbPerLane + e);
+      d[e] = idx >= stop ? ld_volatile(&lb[idx]) : kFlagInc;
+    }
+    int first_inc = kLbPerLane, first_zero = kLbPerLane;
+#pragma unroll
+    for (int e = kLbPerLane - 1; e >= 0; --e) {
+      const u64 f = d[e] >> 62;
+      if (f == 2) first_inc = e;
+      if (f == 0) first_zero = e;
+    }
+    const uint32_t inc_mask = __ballot_sync(0xffffffffu, first_inc < kLbPerLane);
+    const int L = inc_mask ? __ffs(inc_mask) - 1 : 32;
+    const int e_inc = __shfl_sync(0xffffffffu, first_inc, L & 31);
+    // a descriptor nearer than the nearest inclusive one is still unpublished
+    const bool gap = (lane < L && first_zero < kLbPerLane) || (lane == L && first_zero < e_inc);
+    if (__any_sync(0xffffffffu, gap)) {
+      __nanosleep(64);
+      continue;
+    }
+    u64 sum = 0;
+#pragma unroll
+    for (int e = 0; e < kLbPerLane; ++e)
+      if (lane < L || (lane == L && e <= e_inc)) sum += d[e] & kValMask;
+    excl += warp_sum64(sum);
+    if (inc_mask) return excl;
+    base -= 32 * kLbPerLane;
+  }
+}
+
 __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
                                               StageMeta *meta) {
   const int lane = threadIdx.x & 31;
@@ -138,26 +183,7 @@ __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *agg
     if (t == kDone) return;
     if (m.kind == KIND_PARTITION && m.k > 0) {
       const u64 agg = m.agg;
-      u64 excl = 0;
-      long long base = (long long)t - 1;
-      const long long stop = (long long)m.tile_base;
-      for (;;) {
-        const long long idx = base - lane;
-        u64 d = kFlagInc;
-        if (idx >= stop) {
-          do {
-            d = ld_volatile(&lb[idx]);
-          } while ((d >> 62) == 0);
-        }
-        const uint32_t inc = __ballot_sync(0xffffffffu, (d >> 62) == 2);
-        if (inc) {
-          const int first = __ffs(inc) - 1;
-          excl += warp_sum64(lane <= first ? (d & kValMask) : 0ull);
-          break;
-        }
-        excl += warp_sum64(d & kValMask);
-        base -= 32;
-      }
+      const u64 excl = lookback_window(lb, (long long)t - 1, (long long)m.tile_base);
       if (lane == 0) {
         st_volatile(&lb[t], kFlagInc | (excl + agg));
         TSQ_MARK(level, t, 4);
