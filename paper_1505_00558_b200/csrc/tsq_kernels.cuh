@@ -37,8 +37,9 @@ namespace tsq {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;   // 256
 constexpr int kProducerWarp = kConsumerWarps;     // warp 8: tile claims + bulk loads
-constexpr int kLookbackWarp = kConsumerWarps + 1; // warp 9: decoupled look-back
-constexpr int kPartThreads = kConsumers + 64;
+constexpr int kLookbackWarp = kConsumerWarps + 1; // warps 9..: decoupled look-back
+constexpr int kLookbackWarps = 2;                 // alternate stages between them
+constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps);
 constexpr int kStages = 4;                        // input ring depth
 constexpr int kAlign = 4;                         // bulk-copy element alignment
 constexpr int kOutPad = 16;                       // alignment slack of the out buffer

@@ -153,10 +153,21 @@ __device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long lon
     const uint32_t inc_mask = __ballot_sync(0xffffffffu, first_inc < kLbPerLane);
     const int L = inc_mask ? __ffs(inc_mask) - 1 : 32;
     const int e_inc = __shfl_sync(0xffffffffu, first_inc, L & 31);
-    // a descriptor nearer than the nearest inclusive one is still unpublished
+    // a descriptor nearer than the nearest inclusive one is still unpublished:
+    // spin on the nearest such descriptor alone, then re-read the window
     const bool gap = (lane < L && first_zero < kLbPerLane) || (lane == L && first_zero < e_inc);
-    if (__any_sync(0xffffffffu, gap)) {
-      __nanosleep(64);
+    const uint32_t gap_mask = __ballot_sync(0xffffffffu, gap);
+    if (gap_mask) {
+      const int gl = __ffs(gap_mask) - 1;
+      if (lane == gl) {
+        const u64 *p = &lb[base - (gl * kLbPerLane + first_zero)];
+        unsigned ns = 32;
+        while ((ld_volatile(p) >> 62) == 0) {
+          __nanosleep(ns);
+          ns = ns < 256 ? ns * 2 : ns;
+        }
+      }
+      __syncwarp();
       continue;
     }
     u64 sum = 0;
@@ -170,12 +181,14 @@ __device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long lon
 }
 
 __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
-                                              StageMeta *meta) {
+                                              StageMeta *meta, int lw) {
   const int lane = threadIdx.x & 31;
   u64 *lb = P->lookback[cur];
   const uint32_t level = P->ctl->level;
   (void)level;
-  for (uint32_t it = 0;; ++it) {
+  // look-back warp lw owns every kLookbackWarps-th tile of this CTA, so a
+  // slow walk back delays only its own tiles
+  for (uint32_t it = (uint32_t)lw;; it += kLookbackWarps) {
     const int s = (int)(it % kStages);
     wait_aggr_lookback(&aggr[s], (it / kStages) & 1u);
     StageMeta &m = meta[s];
@@ -288,7 +301,14 @@ __device__ __forceinline__ bool classify_tile(const Params *P, int cur, uint32_t
   // stores finished reading the out buffer, which the next emit restages.
   if (t == kDone) {
     if (tid == 0) {
-      mbar_arrive(&aggr[ts.s]);  // lets the look-back warp see the end
+      // every look-back warp must see an end marker: this stage's and, for
+      // the others, the next ones (their last fills were emitted already)
+      mbar_arrive(&aggr[ts.s]);
+      for (uint32_t e = 1; e < (uint32_t)kLookbackWarps; ++e) {
+        const int se = (int)((it + e) % kStages);
+        meta[se].t = kDone;
+        mbar_arrive(&aggr[se]);
+      }
       bulk_wait_read0();
     }
     named_sync(1, kConsumers);
@@ -495,8 +515,8 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
     producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
     return;
   }
-  if (warp == kLookbackWarp) {
-    lookback_loop(P, cur, aggr, ready, meta);
+  if (warp >= kLookbackWarp) {
+    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp);
     return;
   }
   TileState<G::IPT> a, b;
