@@ -1,0 +1,341 @@
+// tsq_consume.cuh -- consumer warps and the partition kernel entry.
+// Included by tsq_partition.cuh after the producer and look-back warps.
+//
+// Consumers handle each tile twice, two tiles apart:
+//   count (tile k+2)  each warp counts the <, ==, > keys it owns -- no CTA
+//                     barrier; the last warp to finish publishes the tile's
+//                     aggregate for the look-back, as early as possible after
+//                     the tile landed (a tile whose aggregate is missing
+//                     stalls every later tile's look-back in its segment)
+//   emit (tile k)     once the look-back warp delivered the tile's offsets:
+//                     rank every key in its class with __ballot_sync /
+//                     __popc, stage the < run and the > run (records: also
+//                     the == payloads) in shared memory aligned like their
+//                     destinations, hand the stage back to the producer and
+//                     write the runs with cp.async.bulk stores (scalar stores
+//                     for the <= 3 unaligned keys at each end)
+#pragma once
+
+namespace tsq {
+
+constexpr int kSkew = kStages - 2;  // tiles counted ahead of the one emitted
+
+// Write one staged run: element j of the run (global index D + j) sits at
+// R[(D & 3) + j]; the 16B-aligned body goes out as one bulk store issued by
+// `issuer`, the <= 3 keys at each ragged end as scalar stores by lanes < 8
+// of warp `scal_warp`.
+template <typename T>
+__device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T *R,
+                                         bool issuer, int scal_warp) {
+  if (L <= 0) return;
+  const long long b0 = (D + kAlign - 1) & ~(long long)(kAlign - 1);
+  const long long b1 = (D + L) & ~(long long)(kAlign - 1);
+  const long long base = D & ~(long long)(kAlign - 1);
+  const bool body = b1 > b0;
+  if (body && issuer)
+    bulk_store(g + b0, R + (b0 - base), (uint32_t)((b1 - b0) * (long long)sizeof(T)));
+  if ((int)(threadIdx.x >> 5) == scal_warp) {
+    const int lane = threadIdx.x & 31;
+    const long long h = body ? (b0 - D) : L;   // head count (all if no body)
+    const long long ts = body ? (b1 - D) : L;  // tail start
+    const long long e = lane < h ? lane : ts + (lane - h);
+    if (lane < 8 && (lane < h || e < L)) g[D + e] = R[(D - base) + e];
+  }
+}
+
+// per-stage bookkeeping shared by the consumer warps
+struct StageCounts {
+  uint32_t w[kConsumerWarps][3];  // per warp: <, ==, > keys
+  uint32_t arrived;               // warps done counting
+  uint32_t bad;                   // verification: a pair out of order
+};
+
+// class of key x against the pivot: 0 <, 1 ==, 2 >, 3 outside the segment
+template <typename U>
+__device__ __forceinline__ uint32_t key_class(U x, U piv, bool valid) {
+  return ((uint32_t)(x >= piv) + (uint32_t)(x > piv)) | (valid ? 0u : 3u);
+}
+
+// Count phase of tile `it`.  Returns false at the end-of-level marker.
+template <class C, bool PAY>
+__device__ __forceinline__ bool count_tile(const Params *P, int cur, uint32_t it,
+                                           const typename C::U *in_k, u64 *full, u64 *aggr,
+                                           StageMeta *meta, StageCounts *sc) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int s = (int)(it % kStages);
+  wait_full_consumer(&full[s], (it / kStages) & 1u);
+  const StageMeta &m = meta[s];
+  const uint32_t t = m.t;
+  if (t == kDone) {
+    if (tid == 0) {
+      // every look-back warp must see an end marker: this stage's and, for
+      // the others, the next ones (their last fills were emitted already)
+      mbar_arrive(&aggr[s]);
+      for (uint32_t e = 1; e < (uint32_t)kLookbackWarps; ++e) {
+        const int se = (int)((it + e) % kStages);
+        meta[se].t = kDone;
+        mbar_arrive(&aggr[se]);
+      }
+    }
+    return false;
+  }
+  const uint32_t level = P->ctl->level;
+  (void)level;
+  if (tid == 0) TSQ_MARK(level, t, 2);
+  const U *sk = in_k + (size_t)s * G::TILE;
+  const bool raw = P->raw[m.buf] != 0;
+  const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
+  StageCounts &c = sc[s];
+  if (m.kind != KIND_PARTITION) {
+    // verification: every owned pair (i, i+1) inside the segment, the last
+    // one against the first key of the next tile
+    bool bad = false;
+    if (!m.skip) {
+      const bool asc = m.kind == KIND_VERIFY_ASC;
+#pragma unroll
+      for (int v = 0; v < G::VPT; ++v) {
+#pragma unroll
+        for (int q = 0; q < G::VN; ++q) {
+          const int i = (v * kConsumers + tid) * G::VN + q;
+          if (i < rlo || i >= rhi) continue;
+          U a = sk[i], b;
+          bool have = true;
+          if (i + 1 < rhi) b = sk[i + 1];
+          else if (m.has_next) b = (U)m.next_key;
+          else have = false;
+          if (raw) {
+            a = C::enc(a);
+            if (i + 1 < rhi) b = C::enc(b);
+          }
+          if (have) bad |= asc ? (a > b) : (a < b);
+        }
+      }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (bad) atomicOr(&c.bad, 1u);
+      __threadfence_block();
+      if (atomicAdd(&c.arrived, 1u) == kConsumerWarps - 1) {
+        if (atomicExch(&c.bad, 0u)) atomicOr(&P->segs[cur][m.sid].fail, 1u);
+        c.arrived = 0;
+        mbar_arrive(&aggr[s]);
+      }
+    }
+    return true;
+  }
+  const U piv = (U)m.pivot;
+  const bool full_tile = rlo == 0 && rhi == G::TILE;
+  uint32_t lt = 0, gt = 0, va = 0;
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + tid) * G::VN;
+    U key[G::VN];
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) {
+      const int idx = e0 + q;
+      const U x = raw ? C::enc(key[q]) : key[q];
+      const bool valid = full_tile || (idx >= rlo && idx < rhi);
+      lt += (valid && x < piv) ? 1u : 0u;
+      gt += (valid && x > piv) ? 1u : 0u;
+      va += valid ? 1u : 0u;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lt += __shfl_xor_sync(0xffffffffu, lt, o);
+    gt += __shfl_xor_sync(0xffffffffu, gt, o);
+    va += __shfl_xor_sync(0xffffffffu, va, o);
+  }
+  if (lane == 0) {
+    c.w[warp][0] = lt;
+    c.w[warp][1] = va - lt - gt;
+    c.w[warp][2] = gt;
+    __threadfence_block();
+    if (atomicAdd(&c.arrived, 1u) == kConsumerWarps - 1) {
+      // last warp: the tile's aggregate
+      uint32_t tl = 0, tg = 0;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        tl += *(volatile uint32_t *)&c.w[w][0];
+        tg += *(volatile uint32_t *)&c.w[w][2];
+      }
+      c.arrived = 0;
+      const u64 agg = ((u64)tl << 31) | (u64)tg;
+      meta[s].agg = agg;
+      st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
+      TSQ_MARK(level, t, 3);
+      mbar_arrive(&aggr[s]);
+    }
+  }
+  return true;
+}
+
+// Emit phase of tile `it`: offsets from the look-back warp, ranks, staging,
+// bulk stores.  `out` alternates between two buffers by tile parity.
+template <class C, bool PAY>
+__device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const typename C::U *in_k,
+                                          const uint32_t *in_p, u64 *ready, u64 *empty,
+                                          StageMeta *meta, const StageCounts *sc,
+                                          typename C::U *ok, uint32_t *op) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int s = (int)(it % kStages);
+  wait_ready_consumer(&ready[s], (it / kStages) & 1u);
+  const StageMeta &m = meta[s];
+  const uint32_t level = P->ctl->level;
+  (void)level;
+  if (m.kind != KIND_PARTITION) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    return;
+  }
+  const uint32_t t = m.t;
+  (void)t;
+  if (tid == 0) TSQ_MARK(level, t, 6);
+  const StageCounts &c = sc[s];
+  uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) {
+    const uint32_t a = c.w[w][0], b = c.w[w][1], d = c.w[w][2];
+    if (w < warp) { w_lt += a; w_eq += b; w_gt += d; }
+    t_lt += a; t_eq += b; t_gt += d;
+  }
+  const u64 ex = m.excl;
+  const int sb = (int)m.buf, db = sb ^ 1;
+  const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
+  const long long begin = m.begin, lo = m.lo;
+  const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
+  const long long D_lt = begin + ex_lt;                  // first slot of this tile's < run
+  const long long D_gt = m.end - ex_gt - (long long)t_gt;  // first slot of its > run
+  const long long D_eq = lo - ex_lt - ex_gt;             // records: side-buffer slot
+  const int o_lt = (int)(D_lt & (kAlign - 1));
+  const int g_base = (o_lt + (int)t_lt + kAlign - 1) & ~(kAlign - 1);
+  const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
+  const int e_base = (o_gt + (int)t_gt + kAlign - 1) & ~(kAlign - 1);
+  const int o_eq = e_base + (int)(D_eq & (kAlign - 1));
+  const U *sk = in_k + (size_t)s * G::TILE;
+  const uint32_t *sp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
+  const U piv = (U)m.pivot;
+  const int rlo = (int)(lo - m.tstart), rhi = (int)(m.hi - m.tstart);
+  const bool full_tile = rlo == 0 && rhi == G::TILE;
+  const uint32_t lmask = (1u << lane) - 1u;
+  uint32_t lt0 = (uint32_t)o_lt + w_lt;                  // next < slot of this warp
+  uint32_t gt0 = (uint32_t)o_gt + t_gt - 1u - w_gt;      // next > slot (filled backwards)
+  uint32_t eq0 = (uint32_t)o_eq + w_eq;
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + tid) * G::VN;
+    U key[G::VN];
+    uint32_t pay[G::VN];
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay);
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) {
+      const int idx = e0 + q;
+      const U x = src_raw ? C::enc(key[q]) : key[q];
+      const uint32_t cl = key_class<U>(x, piv, full_tile || (idx >= rlo && idx < rhi));
+      const uint32_t blt = __ballot_sync(0xffffffffu, cl == 0);
+      const uint32_t bgt = __ballot_sync(0xffffffffu, cl == 2);
+      const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, cl == 1) : 0u;
+      // branch-free slot selection, predicated stores
+      const uint32_t p_lt = lt0 + __popc(blt & lmask);
+      const uint32_t p_gt = gt0 - __popc(bgt & lmask);
+      uint32_t pos = cl == 0u ? p_lt : p_gt;
+      if (PAY) pos = cl == 1u ? eq0 + __popc(beq & lmask) : pos;
+      U y = key[q];
+      if (src_raw != dst_raw) y = src_raw ? C::enc(y) : C::dec(y);
+      if ((cl & 1u) == 0u) ok[pos] = y;  // cl == 0 or cl == 2
+      if (PAY && cl != 3u) op[pos] = pay[q];
+      lt0 += __popc(blt);
+      gt0 -= __popc(bgt);
+      if (PAY) eq0 += __popc(beq);
+    }
+  }
+  // the stage is no longer needed: hand it back to the producer
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&empty[s]);
+  fence_proxy_async_smem();
+  // the previous tile's bulk stores must be done reading the other out
+  // buffer before the next tile restages it (after this barrier)
+  if (tid == 0) bulk_wait_read0();
+  named_sync(1, kConsumers);
+  U *dst = reinterpret_cast<U *>(P->keys[db]);
+  const bool issuer = tid == 0;
+  emit_run<U>(dst, D_lt, t_lt, ok, issuer, 1);
+  emit_run<U>(dst, D_gt, t_gt, ok + g_base, issuer, 2);
+  if (PAY) {
+    uint32_t *dpay = P->pay[db];
+    emit_run<uint32_t>(dpay, D_lt, t_lt, op, issuer, 3);
+    emit_run<uint32_t>(dpay, D_gt, t_gt, op + g_base, issuer, 4);
+    emit_run<uint32_t>(P->side_pay, D_eq, t_eq, op + e_base, issuer, 5);
+  }
+  if (issuer) {
+    bulk_commit();
+    TSQ_MARK(level, t, 7);
+  }
+}
+
+template <class C, bool PAY>
+__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ P) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  U *in_k = reinterpret_cast<U *>(smem_raw);
+  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)kStages * G::TILE);
+  unsigned char *outb = smem_raw + (size_t)kStages * G::STAGE_BYTES;
+  __shared__ __align__(8) u64 full[kStages], aggr[kStages], ready[kStages], empty[kStages];
+  __shared__ StageMeta meta[kStages];
+  __shared__ StageCounts sc[kStages];
+
+  Ctl *ctl = P->ctl;
+  const uint32_t level = ctl->level;
+  const int cur = (int)(level & 1u);
+  const uint32_t ntiles = ctl->cur_ntiles;
+  if (threadIdx.x < kStages) {
+    StageCounts &c = sc[threadIdx.x];
+    c.arrived = 0;
+    c.bad = 0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&aggr[s], 1);
+      mbar_init(&ready[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  if (warp == kProducerWarp) {
+    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
+    return;
+  }
+  if (warp >= kLookbackWarp) {
+    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp);
+    return;
+  }
+  uint32_t done_at = 0xffffffffu;
+  for (uint32_t j = 0; j < (uint32_t)kSkew; ++j)
+    if (!count_tile<C, PAY>(P, cur, j, in_k, full, aggr, meta, sc)) {
+      done_at = j;
+      break;
+    }
+  for (uint32_t k = 0; k < done_at; ++k) {
+    if (k + kSkew < done_at &&
+        !count_tile<C, PAY>(P, cur, k + kSkew, in_k, full, aggr, meta, sc))
+      done_at = k + kSkew;
+    unsigned char *ob = outb + (size_t)(k & 1u) * (G::OUT_K + G::OUT_P);
+    emit_tile<C, PAY>(P, k, in_k, in_p, ready, empty, meta, sc, reinterpret_cast<U *>(ob),
+                      reinterpret_cast<uint32_t *>(ob + G::OUT_K));
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+}  // namespace tsq

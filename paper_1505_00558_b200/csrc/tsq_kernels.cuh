@@ -56,7 +56,7 @@ struct Geo {
   static constexpr size_t STAGE_BYTES = (size_t)TILE * (KB + (PAY ? 4 : 0));
   static constexpr size_t OUT_K = (size_t)(TILE + kOutPad) * KB;
   static constexpr size_t OUT_P = PAY ? (size_t)(TILE + kOutPad) * 4 : 0;
-  static constexpr size_t SMEM = (size_t)kStages * STAGE_BYTES + OUT_K + OUT_P;
+  static constexpr size_t SMEM = (size_t)kStages * STAGE_BYTES + 2 * (OUT_K + OUT_P);
 };
 
 __device__ __forceinline__ void unpack(const uint4 &v, uint32_t *o) {

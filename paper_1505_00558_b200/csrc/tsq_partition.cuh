@@ -210,326 +210,6 @@ __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *agg
   }
 }
 
-// ---------------------------------------------------------------------------
-// Consumers.
-
-// Write one staged run: element j of the run (global index D + j) sits at
-// R[(D & 3) + j]; the 16B-aligned body goes out as one bulk store issued by
-// `issuer`, the <= 3 keys at each ragged end as scalar stores by lanes < 8
-// of warp `scal_warp`.
-template <typename T>
-__device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T *R,
-                                         bool issuer, int scal_warp) {
-  if (L <= 0) return;
-  const long long b0 = (D + kAlign - 1) & ~(long long)(kAlign - 1);
-  const long long b1 = (D + L) & ~(long long)(kAlign - 1);
-  const long long base = D & ~(long long)(kAlign - 1);
-  const bool body = b1 > b0;
-  if (body && issuer)
-    bulk_store(g + b0, R + (b0 - base), (uint32_t)((b1 - b0) * (long long)sizeof(T)));
-  if ((int)(threadIdx.x >> 5) == scal_warp) {
-    const int lane = threadIdx.x & 31;
-    const long long h = body ? (b0 - D) : L;   // head count (all if no body)
-    const long long ts = body ? (b1 - D) : L;  // tail start
-    const long long e = lane < h ? lane : ts + (lane - h);
-    if (lane < 8 && (lane < h || e < L)) g[D + e] = R[(D - base) + e];
-  }
-}
-
-// What the consumers carry from classifying a tile to emitting it.
-template <int IPT>
-struct TileState {
-  int s;
-  uint32_t par;
-  uint32_t partition;  // 0 for a verification tile
-  uint32_t t_lt, t_gt, t_eq, w_lt, w_gt, w_eq;
-  uint32_t cls[IPT];   // class (0 <, 1 ==, 2 >, 3 none) << 16 | rank in class
-};
-
-// one verification tile: every adjacent pair inside the tile and the pair
-// that crosses into the next tile must be ordered; a violation marks the
-// segment failed (its later tiles are skipped by the producer)
-template <class C, bool PAY>
-__device__ __forceinline__ void verify_tile(const Params *P, int cur, const StageMeta &m,
-                                            const typename C::U *sk, uint32_t *s_flag) {
-  typedef typename C::U U;
-  const int tid = threadIdx.x;
-  const bool raw = P->raw[m.buf] != 0;
-  const bool asc = m.kind == KIND_VERIFY_ASC;
-  const long long rlo = m.lo - m.tstart, rhi = m.hi - m.tstart;
-  bool bad = false;
-  if (!m.skip) {
-    for (long long i = rlo + tid; i < rhi; i += kConsumers) {
-      U a = sk[i];
-      U b;
-      bool have = true;
-      if (i + 1 < rhi) b = sk[i + 1];
-      else if (m.has_next) b = (U)m.next_key;
-      else have = false;
-      if (raw) {
-        a = C::enc(a);
-        if (i + 1 < rhi) b = C::enc(b);
-      }
-      if (have) bad |= asc ? (a > b) : (a < b);
-    }
-  }
-  if (tid == 0) *s_flag = 0;
-  named_sync(1, kConsumers);
-  if (bad) *s_flag = 1;
-  named_sync(1, kConsumers);
-  if (tid == 0 && *s_flag) atomicOr(&P->segs[cur][m.sid].fail, 1u);
-}
-
-// Phase A of tile `it`: classify and rank every key, publish the aggregate.
-// Returns false at the end-of-level marker.
-template <class C, bool PAY>
-__device__ __forceinline__ bool classify_tile(const Params *P, int cur, uint32_t it,
-                                              const typename C::U *in_k, u64 *full, u64 *aggr,
-                                              StageMeta *meta, uint32_t (*wcnt)[3],
-                                              uint32_t *s_flag, TileState<Geo<C, PAY>::IPT> &ts) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  ts.s = (int)(it % kStages);
-  ts.par = (it / kStages) & 1u;
-  wait_full_consumer(&full[ts.s], ts.par);
-  const StageMeta &m = meta[ts.s];
-  const uint32_t t = m.t;
-  // Every path through here ends with a consumer barrier that thread 0
-  // (the bulk-store issuer) reaches only after the previous tile's bulk
-  // stores finished reading the out buffer, which the next emit restages.
-  if (t == kDone) {
-    if (tid == 0) {
-      // every look-back warp must see an end marker: this stage's and, for
-      // the others, the next ones (their last fills were emitted already)
-      mbar_arrive(&aggr[ts.s]);
-      for (uint32_t e = 1; e < (uint32_t)kLookbackWarps; ++e) {
-        const int se = (int)((it + e) % kStages);
-        meta[se].t = kDone;
-        mbar_arrive(&aggr[se]);
-      }
-      bulk_wait_read0();
-    }
-    named_sync(1, kConsumers);
-    return false;
-  }
-  const U *sk = in_k + (size_t)ts.s * G::TILE;
-  const uint32_t level = P->ctl->level;
-  (void)level;
-  if (tid == 0) TSQ_MARK(level, t, 2);
-  if (m.kind != KIND_PARTITION) {
-    ts.partition = 0;
-    if (tid == 0) bulk_wait_read0();
-    verify_tile<C, PAY>(P, cur, m, sk, s_flag);
-    if (tid == 0) mbar_arrive(&aggr[ts.s]);
-    return true;
-  }
-  ts.partition = 1;
-  const bool src_raw = P->raw[m.buf] != 0;
-  const U piv = (U)m.pivot;
-  const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
-  const bool full_tile = rlo == 0 && rhi == G::TILE;
-#pragma unroll
-  for (int v = 0; v < G::VPT; ++v) {
-    const int e0 = (v * kConsumers + tid) * G::VN;
-    U key[G::VN];
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
-#pragma unroll
-    for (int q = 0; q < G::VN; ++q) {
-      const int idx = e0 + q;
-      const U x = src_raw ? C::enc(key[q]) : key[q];
-      const uint32_t valid = (full_tile || (idx >= rlo && idx < rhi)) ? 1u : 0u;
-      // 0 <, 1 ==, 2 >, 3 outside the segment (branch-free)
-      const uint32_t c = ((uint32_t)(x >= piv) + (uint32_t)(x > piv)) | ((valid ^ 1u) * 3u);
-      ts.cls[v * G::VN + q] = c;
-    }
-  }
-  // warp-level ranks per class, ordered by (item, lane); masks select the
-  // class's ballot and running count without branches
-  const uint32_t lmask = (1u << lane) - 1u;
-  uint32_t lt_run = 0, gt_run = 0, eq_run = 0;
-#pragma unroll
-  for (int i = 0; i < G::IPT; ++i) {
-    const uint32_t c = ts.cls[i];
-    const uint32_t blt = __ballot_sync(0xffffffffu, c == 0);
-    const uint32_t bgt = __ballot_sync(0xffffffffu, c == 2);
-    const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, c == 1) : 0u;
-    const uint32_t mlt = 0u - (uint32_t)(c == 0), mgt = 0u - (uint32_t)(c == 2);
-    const uint32_t meq = PAY ? 0u - (uint32_t)(c == 1) : 0u;
-    const uint32_t bm = (blt & mlt) | (bgt & mgt) | (beq & meq);
-    const uint32_t base = (lt_run & mlt) | (gt_run & mgt) | (eq_run & meq);
-    ts.cls[i] = (c << 16) | (base + __popc(bm & lmask));
-    lt_run += __popc(blt);
-    gt_run += __popc(bgt);
-    if (PAY) eq_run += __popc(beq);
-  }
-  uint32_t(*wc)[3] = wcnt + (it & 1u) * kConsumerWarps;
-  if (lane == 0) {
-    wc[warp][0] = lt_run;
-    wc[warp][1] = eq_run;
-    wc[warp][2] = gt_run;
-  }
-  // the previous tile's bulk stores must have finished reading the out
-  // buffer before the tile after this barrier restages it
-  if (tid == 0) bulk_wait_read0();
-  named_sync(1, kConsumers);
-  uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
-#pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) {
-    const uint32_t a = wc[w][0], b = wc[w][1], c = wc[w][2];
-    if (w < warp) { w_lt += a; w_eq += b; w_gt += c; }
-    t_lt += a; t_eq += b; t_gt += c;
-  }
-  ts.w_lt = w_lt; ts.w_eq = w_eq; ts.w_gt = w_gt;
-  ts.t_lt = t_lt; ts.t_eq = t_eq; ts.t_gt = t_gt;
-  if (tid == 0) {
-    const u64 agg = ((u64)t_lt << 31) | (u64)t_gt;
-    StageMeta &mw = meta[ts.s];
-    mw.agg = agg;
-    st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
-    TSQ_MARK(level, t, 3);
-    mbar_arrive(&aggr[ts.s]);
-  }
-  return true;
-}
-
-// Phase B of a tile: wait for its offsets, stage its runs, write them out.
-template <class C, bool PAY>
-__device__ __forceinline__ void emit_tile(const Params *P, const typename C::U *in_k,
-                                          const uint32_t *in_p, u64 *ready, u64 *empty,
-                                          StageMeta *meta, typename C::U *ok, uint32_t *op,
-                                          const TileState<Geo<C, PAY>::IPT> &ts) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  if (!ts.partition) {
-    // the look-back warp still walks this stage's meta: wait for it (this
-    // also keeps the aggr / ready phases of a stage from running ahead)
-    wait_ready_consumer(&ready[ts.s], ts.par);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[ts.s]);
-    return;
-  }
-  const StageMeta &m = meta[ts.s];
-  const uint32_t level = P->ctl->level;
-  (void)level;
-  if (tid == 0) TSQ_MARK(level, m.t, 5);
-  wait_ready_consumer(&ready[ts.s], ts.par);
-  if (tid == 0) TSQ_MARK(level, m.t, 6);
-  const u64 ex = m.excl;
-  const int sb = (int)m.buf, db = sb ^ 1;
-  const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
-  const long long begin = m.begin, end = m.end, lo = m.lo;
-  const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
-  const long long D_lt = begin + ex_lt;                      // first slot of this tile's < run
-  const long long D_gt = end - ex_gt - (long long)ts.t_gt;   // first slot of its > run
-  const long long D_eq = begin + (lo - begin) - ex_lt - ex_gt;  // records: side-buffer slot
-  const int o_lt = (int)(D_lt & (kAlign - 1));
-  const int g_base = (o_lt + (int)ts.t_lt + kAlign - 1) & ~(kAlign - 1);
-  const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
-  const int e_base = (o_gt + (int)ts.t_gt + kAlign - 1) & ~(kAlign - 1);
-  const int o_eq = e_base + (int)(D_eq & (kAlign - 1));
-  const U *sk = in_k + (size_t)ts.s * G::TILE;
-  const uint32_t *sp = PAY ? in_p + (size_t)ts.s * G::TILE : nullptr;
-  const uint32_t lt0 = (uint32_t)o_lt + ts.w_lt;
-  const uint32_t gt0 = (uint32_t)o_gt + ts.t_gt - 1u - ts.w_gt;
-  const uint32_t eq0 = (uint32_t)o_eq + ts.w_eq;
-#pragma unroll
-  for (int v = 0; v < G::VPT; ++v) {
-    const int e0 = (v * kConsumers + tid) * G::VN;
-    U key[G::VN];
-    uint32_t pay[G::VN];
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
-    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay);
-#pragma unroll
-    for (int q = 0; q < G::VN; ++q) {
-      // branch-free: select the slot, predicate the stores
-      const uint32_t cr = ts.cls[v * G::VN + q];
-      const uint32_t c = cr >> 16, rk = cr & 0xffffu;
-      const uint32_t p_lt = lt0 + rk;
-      const uint32_t p_gt = gt0 - rk;  // > run fills backwards
-      uint32_t pos = c == 0u ? p_lt : p_gt;
-      if (PAY) pos = c == 1u ? eq0 + rk : pos;
-      U x = key[q];
-      if (src_raw != dst_raw) x = src_raw ? C::enc(x) : C::dec(x);
-      if ((c & 1u) == 0u) ok[pos] = x;   // c == 0 or c == 2
-      if (PAY && c != 3u) op[pos] = pay[q];
-    }
-  }
-  const uint32_t t = m.t;
-  (void)t;
-  // the stage is no longer needed: hand it back to the producer
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&empty[ts.s]);
-  fence_proxy_async_smem();
-  named_sync(1, kConsumers);
-  U *dst = reinterpret_cast<U *>(P->keys[db]);
-  const bool issuer = tid == 0;
-  emit_run<U>(dst, D_lt, ts.t_lt, ok, issuer, 1);
-  emit_run<U>(dst, D_gt, ts.t_gt, ok + g_base, issuer, 2);
-  if (PAY) {
-    uint32_t *dpay = P->pay[db];
-    emit_run<uint32_t>(dpay, D_lt, ts.t_lt, op, issuer, 3);
-    emit_run<uint32_t>(dpay, D_gt, ts.t_gt, op + g_base, issuer, 4);
-    emit_run<uint32_t>(P->side_pay, D_eq, ts.t_eq, op + e_base, issuer, 5);
-  }
-  if (issuer) {
-    bulk_commit();
-    TSQ_MARK(level, t, 7);
-  }
-}
-
-template <class C, bool PAY>
-__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ P) {
-  typedef typename C::U U;
-  typedef Geo<C, PAY> G;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  U *in_k = reinterpret_cast<U *>(smem_raw);
-  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)kStages * G::TILE);
-  U *out_k = reinterpret_cast<U *>(smem_raw + (size_t)kStages * G::STAGE_BYTES);
-  uint32_t *out_p = reinterpret_cast<uint32_t *>(smem_raw + (size_t)kStages * G::STAGE_BYTES +
-                                                 G::OUT_K);
-  __shared__ __align__(8) u64 full[kStages], aggr[kStages], ready[kStages], empty[kStages];
-  __shared__ StageMeta meta[kStages];
-  __shared__ uint32_t wcnt[2 * kConsumerWarps][3];
-  __shared__ uint32_t s_flag;
-
-  Ctl *ctl = P->ctl;
-  const uint32_t level = ctl->level;
-  const int cur = (int)(level & 1u);
-  const uint32_t ntiles = ctl->cur_ntiles;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&aggr[s], 1);
-      mbar_init(&ready[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  if (warp == kProducerWarp) {
-    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
-    return;
-  }
-  if (warp >= kLookbackWarp) {
-    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp);
-    return;
-  }
-  TileState<G::IPT> a, b;
-  bool more = classify_tile<C, PAY>(P, cur, 0, in_k, full, aggr, meta, wcnt, &s_flag, a);
-  for (uint32_t it = 1; more; ++it) {
-    // classify the next tile before emitting this one: its aggregate is
-    // published while this tile's look-back completes
-    const bool next = classify_tile<C, PAY>(P, cur, it, in_k, full, aggr, meta, wcnt, &s_flag, b);
-    emit_tile<C, PAY>(P, in_k, in_p, ready, empty, meta, out_k, out_p, a);
-    if (!next) break;
-    a = b;
-  }
-  if (threadIdx.x == 0) bulk_wait0();
-}
-
 }  // namespace tsq
+
+#include "tsq_consume.cuh"

@@ -40,9 +40,9 @@ tr = tr.reshape(-1, 8)[:nt].astype(np.int64)
 t0 = tr[tr[:, 0] > 0, 0].min()
 tr = np.where(tr > 0, tr - t0, -1)
 print(f"level {level}: {lv}  tiles traced {nt}")
-names = ["resolve(1-0)", "land+lag(2-1)", "classify(3-2)", "lookback(4-3)", "skew(5-3)",
-         "ready_wait(6-5)", "stage+emit(7-6)", "total(7-0)"]
-pairs = [(1, 0), (2, 1), (3, 2), (4, 3), (5, 3), (6, 5), (7, 6), (7, 0)]
+names = ["resolve(1-0)", "land+lag(2-1)", "count(3-2)", "lookback(4-3)", "agg->emit(6-3)",
+         "lb->emit(6-4)", "stage+emit(7-6)", "total(7-0)"]
+pairs = [(1, 0), (2, 1), (3, 2), (4, 3), (6, 3), (6, 4), (7, 6), (7, 0)]
 for name, (a, b) in zip(names, pairs):
     ok = (tr[:, a] >= 0) & (tr[:, b] >= 0)
     x = (tr[ok, a] - tr[ok, b]) / 1000.0
