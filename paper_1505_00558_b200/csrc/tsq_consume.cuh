@@ -1,24 +1,24 @@
-// tsq_consume.cuh -- consumer warps and the partition kernel entry.
-// Included by tsq_partition.cuh after the producer and look-back warps.
+// tsq_consume.cuh -- counter and consumer warps, and the partition kernel
+// entry.  Included by tsq_partition.cuh after the producer and look-back
+// warps.
 //
-// Consumers handle each tile twice, two tiles apart:
-//   count (tile k+2)  each warp counts the <, ==, > keys it owns -- no CTA
-//                     barrier; the last warp to finish publishes the tile's
-//                     aggregate for the look-back, as early as possible after
-//                     the tile landed (a tile whose aggregate is missing
-//                     stalls every later tile's look-back in its segment)
-//   emit (tile k)     once the look-back warp delivered the tile's offsets:
-//                     rank every key in its class with __ballot_sync /
-//                     __popc, stage the < run and the > run (records: also
-//                     the == payloads) in shared memory aligned like their
-//                     destinations, hand the stage back to the producer and
-//                     write the runs with cp.async.bulk stores (scalar stores
-//                     for the <= 3 unaligned keys at each end)
+//   counter warps (2)  take alternate stages as soon as they land and count
+//                      the <, ==, > keys each consumer warp owns; the tile's
+//                      aggregate is published for the look-back right away --
+//                      counting never waits on anything but the data, so a
+//                      landed tile never holds up a later tile's look-back.
+//                      Verification tiles (sorted / reversed fast paths) are
+//                      checked here too.
+//   consumers (8)      once the look-back warp delivered a tile's offsets:
+//                      rank every key in its class with __ballot_sync /
+//                      __popc, stage the < run and the > run (records: also
+//                      the == payloads) in shared memory aligned like their
+//                      destinations, hand the stage back to the producer and
+//                      write the runs with cp.async.bulk stores (scalar
+//                      stores for the <= 3 unaligned keys at each end)
 #pragma once
 
 namespace tsq {
-
-constexpr int kSkew = kStages - 2;  // tiles counted ahead of the one emitted
 
 // Write one staged run: element j of the run (global index D + j) sits at
 // R[(D & 3) + j]; the 16B-aligned body goes out as one bulk store issued by
@@ -43,11 +43,9 @@ __device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T
   }
 }
 
-// per-stage bookkeeping shared by the consumer warps
+// per-stage counts of each consumer warp's keys: <, ==, >
 struct StageCounts {
-  uint32_t w[kConsumerWarps][3];  // per warp: <, ==, > keys
-  uint32_t arrived;               // warps done counting
-  uint32_t bad;                   // verification: a pair out of order
+  uint32_t w[kConsumerWarps][3];
 };
 
 // class of key x against the pivot: 0 <, 1 ==, 2 >, 3 outside the segment
@@ -56,51 +54,32 @@ __device__ __forceinline__ uint32_t key_class(U x, U piv, bool valid) {
   return ((uint32_t)(x >= piv) + (uint32_t)(x > piv)) | (valid ? 0u : 3u);
 }
 
-// Count phase of tile `it`.  Returns false at the end-of-level marker.
 template <class C, bool PAY>
-__device__ __forceinline__ bool count_tile(const Params *P, int cur, uint32_t it,
-                                           const typename C::U *in_k, u64 *full, u64 *aggr,
-                                           StageMeta *meta, StageCounts *sc) {
+__device__ __forceinline__ void counter_loop(const Params *P, int cur, const typename C::U *in_k,
+                                             u64 *full, u64 *aggr, u64 *empty, StageMeta *meta,
+                                             StageCounts *sc, int cw,
+                                             const volatile uint32_t *done_iter) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int s = (int)(it % kStages);
-  wait_full_consumer(&full[s], (it / kStages) & 1u);
-  const StageMeta &m = meta[s];
-  const uint32_t t = m.t;
-  if (t == kDone) {
-    if (tid == 0) {
-      // every look-back warp must see an end marker: this stage's and, for
-      // the others, the next ones (their last fills were emitted already)
-      mbar_arrive(&aggr[s]);
-      for (uint32_t e = 1; e < (uint32_t)kLookbackWarps; ++e) {
-        const int se = (int)((it + e) % kStages);
-        meta[se].t = kDone;
-        mbar_arrive(&aggr[se]);
-      }
-    }
-    return false;
-  }
+  const int lane = threadIdx.x & 31;
   const uint32_t level = P->ctl->level;
   (void)level;
-  if (tid == 0) TSQ_MARK(level, t, 2);
-  const U *sk = in_k + (size_t)s * G::TILE;
-  const bool raw = P->raw[m.buf] != 0;
-  const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
-  StageCounts &c = sc[s];
-  if (m.kind != KIND_PARTITION) {
-    // verification: every owned pair (i, i+1) inside the segment, the last
-    // one against the first key of the next tile
-    bool bad = false;
-    if (!m.skip) {
-      const bool asc = m.kind == KIND_VERIFY_ASC;
-#pragma unroll
-      for (int v = 0; v < G::VPT; ++v) {
-#pragma unroll
-        for (int q = 0; q < G::VN; ++q) {
-          const int i = (v * kConsumers + tid) * G::VN + q;
-          if (i < rlo || i >= rhi) continue;
+  for (uint32_t it = (uint32_t)cw;; it += kCounterWarps) {
+    const int s = (int)(it % kStages);
+    if (!wait_or_done(&full[s], (it / kStages) & 1u, done_iter, it)) return;
+    StageMeta &m = meta[s];
+    const uint32_t t = m.t;
+    if (lane == 0) TSQ_MARK(level, t, 2);
+    const U *sk = in_k + (size_t)s * G::TILE;
+    const bool raw = P->raw[m.buf] != 0;
+    const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
+    if (m.kind != KIND_PARTITION) {
+      // verification: every pair (i, i+1) of the segment's keys in this tile,
+      // the last one against the first key of the next tile
+      bool bad = false;
+      if (!m.skip) {
+        const bool asc = m.kind == KIND_VERIFY_ASC;
+        for (int i = rlo + lane; i < rhi; i += 32) {
           U a = sk[i], b;
           bool have = true;
           if (i + 1 < rhi) b = sk[i + 1];
@@ -113,80 +92,71 @@ __device__ __forceinline__ bool count_tile(const Params *P, int cur, uint32_t it
           if (have) bad |= asc ? (a > b) : (a < b);
         }
       }
-    }
-    bad = __any_sync(0xffffffffu, bad);
-    if (lane == 0) {
-      if (bad) atomicOr(&c.bad, 1u);
-      __threadfence_block();
-      if (atomicAdd(&c.arrived, 1u) == kConsumerWarps - 1) {
-        if (atomicExch(&c.bad, 0u)) atomicOr(&P->segs[cur][m.sid].fail, 1u);
-        c.arrived = 0;
-        mbar_arrive(&aggr[s]);
-      }
-    }
-    return true;
-  }
-  const U piv = (U)m.pivot;
-  const bool full_tile = rlo == 0 && rhi == G::TILE;
-  uint32_t lt = 0, gt = 0, va = 0;
-#pragma unroll
-  for (int v = 0; v < G::VPT; ++v) {
-    const int e0 = (v * kConsumers + tid) * G::VN;
-    U key[G::VN];
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
-#pragma unroll
-    for (int q = 0; q < G::VN; ++q) {
-      const int idx = e0 + q;
-      const U x = raw ? C::enc(key[q]) : key[q];
-      const bool valid = full_tile || (idx >= rlo && idx < rhi);
-      lt += (valid && x < piv) ? 1u : 0u;
-      gt += (valid && x > piv) ? 1u : 0u;
-      va += valid ? 1u : 0u;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lt += __shfl_xor_sync(0xffffffffu, lt, o);
-    gt += __shfl_xor_sync(0xffffffffu, gt, o);
-    va += __shfl_xor_sync(0xffffffffu, va, o);
-  }
-  if (lane == 0) {
-    c.w[warp][0] = lt;
-    c.w[warp][1] = va - lt - gt;
-    c.w[warp][2] = gt;
-    __threadfence_block();
-    if (atomicAdd(&c.arrived, 1u) == kConsumerWarps - 1) {
-      // last warp: the tile's aggregate
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&P->segs[cur][m.sid].fail, 1u);
+    } else {
+      // each consumer warp's keys, in the order it will rank them
+      const U piv = (U)m.pivot;
+      const bool full_tile = rlo == 0 && rhi == G::TILE;
       uint32_t tl = 0, tg = 0;
-#pragma unroll
+#pragma unroll 1
       for (int w = 0; w < kConsumerWarps; ++w) {
-        tl += *(volatile uint32_t *)&c.w[w][0];
-        tg += *(volatile uint32_t *)&c.w[w][2];
+        uint32_t lt = 0, gt = 0, va = 0;
+#pragma unroll
+        for (int v = 0; v < G::VPT; ++v) {
+          const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
+          U key[G::VN];
+          unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+#pragma unroll
+          for (int q = 0; q < G::VN; ++q) {
+            const int idx = e0 + q;
+            const U x = raw ? C::enc(key[q]) : key[q];
+            const bool valid = full_tile || (idx >= rlo && idx < rhi);
+            lt += (valid && x < piv) ? 1u : 0u;
+            gt += (valid && x > piv) ? 1u : 0u;
+            va += valid ? 1u : 0u;
+          }
+        }
+        // at most 32 * IPT = 512 per class: pack three 11-bit counts
+        uint32_t pk = lt | (gt << 11) | (va << 22);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pk += __shfl_xor_sync(0xffffffffu, pk, o);
+        lt = pk & 0x7ffu;
+        gt = (pk >> 11) & 0x7ffu;
+        va = pk >> 22;
+        if (lane == 0) {
+          sc[s].w[w][0] = lt;
+          sc[s].w[w][1] = va - lt - gt;
+          sc[s].w[w][2] = gt;
+        }
+        tl += lt;
+        tg += gt;
       }
-      c.arrived = 0;
-      const u64 agg = ((u64)tl << 31) | (u64)tg;
-      meta[s].agg = agg;
-      st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
-      TSQ_MARK(level, t, 3);
+      if (lane == 0) {
+        const u64 agg = ((u64)tl << 31) | (u64)tg;
+        m.agg = agg;
+        st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
+        TSQ_MARK(level, t, 3);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
       mbar_arrive(&aggr[s]);
+      mbar_arrive(&empty[s]);  // done reading the stage
     }
   }
-  return true;
 }
 
-// Emit phase of tile `it`: offsets from the look-back warp, ranks, staging,
-// bulk stores.  `out` alternates between two buffers by tile parity.
+// Emit one tile: offsets from the look-back warp, ranks, staging, bulk
+// stores.  `ok` / `op` alternate between two buffers by tile parity.
 template <class C, bool PAY>
 __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const typename C::U *in_k,
-                                          const uint32_t *in_p, u64 *ready, u64 *empty,
-                                          StageMeta *meta, const StageCounts *sc,
-                                          typename C::U *ok, uint32_t *op) {
+                                          const uint32_t *in_p, u64 *empty, StageMeta *meta,
+                                          const StageCounts *sc, typename C::U *ok, uint32_t *op) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int s = (int)(it % kStages);
-  wait_ready_consumer(&ready[s], (it / kStages) & 1u);
   const StageMeta &m = meta[s];
   const uint32_t level = P->ctl->level;
   (void)level;
@@ -211,9 +181,9 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const ty
   const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;
   const long long begin = m.begin, lo = m.lo;
   const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
-  const long long D_lt = begin + ex_lt;                  // first slot of this tile's < run
+  const long long D_lt = begin + ex_lt;                    // first slot of this tile's < run
   const long long D_gt = m.end - ex_gt - (long long)t_gt;  // first slot of its > run
-  const long long D_eq = lo - ex_lt - ex_gt;             // records: side-buffer slot
+  const long long D_eq = lo - ex_lt - ex_gt;               // records: side-buffer slot
   const int o_lt = (int)(D_lt & (kAlign - 1));
   const int g_base = (o_lt + (int)t_lt + kAlign - 1) & ~(kAlign - 1);
   const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
@@ -225,8 +195,8 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const ty
   const int rlo = (int)(lo - m.tstart), rhi = (int)(m.hi - m.tstart);
   const bool full_tile = rlo == 0 && rhi == G::TILE;
   const uint32_t lmask = (1u << lane) - 1u;
-  uint32_t lt0 = (uint32_t)o_lt + w_lt;                  // next < slot of this warp
-  uint32_t gt0 = (uint32_t)o_gt + t_gt - 1u - w_gt;      // next > slot (filled backwards)
+  uint32_t lt0 = (uint32_t)o_lt + w_lt;              // next < slot of this warp
+  uint32_t gt0 = (uint32_t)o_gt + t_gt - 1u - w_gt;  // next > slot (filled backwards)
   uint32_t eq0 = (uint32_t)o_eq + w_eq;
 #pragma unroll
   for (int v = 0; v < G::VPT; ++v) {
@@ -292,47 +262,42 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
   __shared__ __align__(8) u64 full[kStages], aggr[kStages], ready[kStages], empty[kStages];
   __shared__ StageMeta meta[kStages];
   __shared__ StageCounts sc[kStages];
+  __shared__ volatile uint32_t done_iter;
 
   Ctl *ctl = P->ctl;
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u);
   const uint32_t ntiles = ctl->cur_ntiles;
-  if (threadIdx.x < kStages) {
-    StageCounts &c = sc[threadIdx.x];
-    c.arrived = 0;
-    c.bad = 0;
-  }
   if (threadIdx.x == 0) {
+    done_iter = 0xffffffffu;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&aggr[s], 1);
       mbar_init(&ready[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], kConsumerWarps + 1);  // consumers + the stage's counter warp
     }
     fence_barrier_init();
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   if (warp == kProducerWarp) {
-    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta);
+    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta, &done_iter);
+    return;
+  }
+  if (warp >= kCounterWarp) {
+    counter_loop<C, PAY>(P, cur, in_k, full, aggr, empty, meta, sc, warp - kCounterWarp,
+                         &done_iter);
     return;
   }
   if (warp >= kLookbackWarp) {
-    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp);
+    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp, &done_iter);
     return;
   }
-  uint32_t done_at = 0xffffffffu;
-  for (uint32_t j = 0; j < (uint32_t)kSkew; ++j)
-    if (!count_tile<C, PAY>(P, cur, j, in_k, full, aggr, meta, sc)) {
-      done_at = j;
-      break;
-    }
-  for (uint32_t k = 0; k < done_at; ++k) {
-    if (k + kSkew < done_at &&
-        !count_tile<C, PAY>(P, cur, k + kSkew, in_k, full, aggr, meta, sc))
-      done_at = k + kSkew;
+  for (uint32_t k = 0;; ++k) {
+    const int s = (int)(k % kStages);
+    if (!wait_or_done(&ready[s], (k / kStages) & 1u, &done_iter, k)) break;
     unsigned char *ob = outb + (size_t)(k & 1u) * (G::OUT_K + G::OUT_P);
-    emit_tile<C, PAY>(P, k, in_k, in_p, ready, empty, meta, sc, reinterpret_cast<U *>(ob),
+    emit_tile<C, PAY>(P, k, in_k, in_p, empty, meta, sc, reinterpret_cast<U *>(ob),
                       reinterpret_cast<uint32_t *>(ob + G::OUT_K));
   }
   if (threadIdx.x == 0) bulk_wait0();

@@ -239,6 +239,28 @@ __device__ __forceinline__ void wait_empty_producer(u64 *bar, uint32_t parity) {
 }
 #undef TSQ_WAIT_ASM
 
+// Wait for phase `parity` of `bar`, unless the level ends first: returns
+// false once *done_iter (the ring iteration at which the producer ran out of
+// tiles; ~0u while running) is <= it.
+__device__ __forceinline__ bool mbar_try_wait(u64 *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 500;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool wait_or_done(u64 *bar, uint32_t parity,
+                                             const volatile uint32_t *done_iter, uint32_t it) {
+  for (;;) {
+    if (mbar_try_wait(bar, parity)) return true;
+    if (it >= *done_iter) return false;
+  }
+}
+
 // 1-D bulk copy global -> shared, completing `bytes` on the mbarrier
 // (cp.async.bulk: SASS UBLKCP); dst/src 16-byte aligned, bytes % 16 == 0
 __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes,

@@ -37,9 +37,11 @@ namespace tsq {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;   // 256
 constexpr int kProducerWarp = kConsumerWarps;     // warp 8: tile claims + bulk loads
-constexpr int kLookbackWarp = kConsumerWarps + 1; // warps 9..: decoupled look-back
+constexpr int kLookbackWarp = kConsumerWarps + 1; // warps 9, 10: decoupled look-back
 constexpr int kLookbackWarps = 2;                 // alternate stages between them
-constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps);
+constexpr int kCounterWarp = kLookbackWarp + kLookbackWarps;  // warps 11, 12: counts
+constexpr int kCounterWarps = 2;
+constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps + kCounterWarps);
 constexpr int kStages = 4;                        // input ring depth
 constexpr int kAlign = 4;                         // bulk-copy element alignment
 constexpr int kOutPad = 16;                       // alignment slack of the out buffer

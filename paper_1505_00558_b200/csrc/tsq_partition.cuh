@@ -35,7 +35,8 @@ namespace tsq {
 template <class C, bool PAY>
 __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t ntiles,
                                               typename C::U *in_k, uint32_t *in_p, u64 *full,
-                                              u64 *empty, StageMeta *meta) {
+                                              u64 *empty, StageMeta *meta,
+                                              volatile uint32_t *done_iter) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   const int lane = threadIdx.x & 31;
@@ -53,10 +54,8 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
     t = __shfl_sync(0xffffffffu, t, 0);
     StageMeta &m = meta[s];
     if (t >= ntiles) {
-      if (lane == 0) {
-        m.t = kDone;
-        mbar_arrive(&full[s]);
-      }
+      // iteration `it` and later have no tile: every role stops there
+      if (lane == 0) *done_iter = it;
       return;
     }
     TSQ_MARK(level, t, 0);
@@ -181,7 +180,8 @@ __device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long lon
 }
 
 __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
-                                              StageMeta *meta, int lw) {
+                                              StageMeta *meta, int lw,
+                                              const volatile uint32_t *done_iter) {
   const int lane = threadIdx.x & 31;
   u64 *lb = P->lookback[cur];
   const uint32_t level = P->ctl->level;
@@ -190,10 +190,9 @@ __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *agg
   // slow walk back delays only its own tiles
   for (uint32_t it = (uint32_t)lw;; it += kLookbackWarps) {
     const int s = (int)(it % kStages);
-    wait_aggr_lookback(&aggr[s], (it / kStages) & 1u);
+    if (!wait_or_done(&aggr[s], (it / kStages) & 1u, done_iter, it)) return;
     StageMeta &m = meta[s];
     const uint32_t t = m.t;
-    if (t == kDone) return;
     if (m.kind == KIND_PARTITION && m.k > 0) {
       const u64 agg = m.agg;
       const u64 excl = lookback_window(lb, (long long)t - 1, (long long)m.tile_base);
