@@ -126,10 +126,11 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t,
 
 /* Per-level trace of the last host_levels sort (the stage_hook / trace
  * analogue, core.py:1705-1710): device ms of the partition pass and of the
- * scheduling pass, live segments and tiles per level.  Returns the number
- * of levels (may exceed cap); any output pointer may be NULL. */
+ * scheduling pass, live segments, tiles and algorithmic HBM bytes of the
+ * partition pass per level.  Returns the number of levels (may exceed cap);
+ * any output pointer may be NULL. */
 int tsq_level_trace(const tsq_workspace *ws, float *part_ms, float *sched_ms,
-                    uint32_t *segments, uint32_t *tiles, int cap);
+                    uint32_t *segments, uint32_t *tiles, uint64_t *bytes, int cap);
 
 /* One stage: three-way partition of keys[0..n) around `pivot` (raw bits of a
  * key of key_t), out of place into out_keys (and out_payload), < from the

@@ -100,7 +100,8 @@ def lib():
         L.tsq_level_trace.argtypes = [vp, ctypes.POINTER(ctypes.c_float),
                                       ctypes.POINTER(ctypes.c_float),
                                       ctypes.POINTER(ctypes.c_uint32),
-                                      ctypes.POINTER(ctypes.c_uint32), i32]
+                                      ctypes.POINTER(ctypes.c_uint32),
+                                      ctypes.POINTER(ctypes.c_uint64), i32]
         L.tsq_level_trace.restype = i32
         _lib = L
     return _lib
@@ -153,7 +154,8 @@ class Workspace:
         sms = (ctypes.c_float * cap)()
         segs = (ctypes.c_uint32 * cap)()
         tiles = (ctypes.c_uint32 * cap)()
-        n = lib().tsq_level_trace(self.handle, ms, sms, segs, tiles, cap)
+        nbytes = (ctypes.c_uint64 * cap)()
+        n = lib().tsq_level_trace(self.handle, ms, sms, segs, tiles, nbytes, cap)
         n = min(n, cap)
-        return [{"ms": ms[i], "sched_ms": sms[i], "segments": segs[i], "tiles": tiles[i]}
-                for i in range(n)]
+        return [{"ms": ms[i], "sched_ms": sms[i], "segments": segs[i], "tiles": tiles[i],
+                 "bytes": nbytes[i]} for i in range(n)]

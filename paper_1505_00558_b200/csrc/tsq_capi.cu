@@ -145,6 +145,7 @@ struct tsq_workspace {
   std::mutex mu;
   std::map<int, GraphEntry> graphs;
   std::vector<float> level_ms, sched_ms;  // host_levels mode trace
+  std::vector<uint64_t> level_bytes;
   std::vector<uint32_t> level_segs, level_tiles;
 };
 
@@ -576,9 +577,15 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   void *largs[1] = {&dst};
   const LevelLaunch LL = level_launch(ws, ks);
   float total_levels = 0.f;
+  ws->level_bytes.clear();
+  u64 bytes_before = 0;
   for (int lv = 0; lv < kMaxLevels; ++lv) {
     st = read_ctl(ws, s);
     if (st != TSQ_OK) return st;
+    if (lv > 0) {  // algorithmic bytes the previous level's partition pass moved
+      ws->level_bytes.push_back(ws->h_ctl->bytes_partition - bytes_before);
+      bytes_before = ws->h_ctl->bytes_partition;
+    }
     if (ws->h_ctl->cur_nseg == 0 || ws->h_ctl->error) break;
     ws->level_segs.push_back(ws->h_ctl->cur_nseg);
     ws->level_tiles.push_back(ws->h_ctl->cur_ntiles);
@@ -618,10 +625,11 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
 }
 
 int tsq_level_trace(const tsq_workspace *ws, float *part_ms, float *sched_ms, uint32_t *segs,
-                    uint32_t *tiles, int cap) {
+                    uint32_t *tiles, uint64_t *bytes, int cap) {
   if (!ws) return 0;
   int n = (int)ws->level_ms.size();
   for (int i = 0; i < n && i < cap; ++i) {
+    if (bytes) bytes[i] = i < (int)ws->level_bytes.size() ? ws->level_bytes[i] : 0;
     if (part_ms) part_ms[i] = ws->level_ms[i];
     if (sched_ms) sched_ms[i] = ws->sched_ms[i];
     if (segs) segs[i] = ws->level_segs[i];
