@@ -38,7 +38,7 @@ KernelSet make_set() {
   s.tile = Geo<C, PAY>::TILE;
   s.part_smem = Geo<C, PAY>::SMEM;
   s.sched_smem = (size_t)(kThreads / 32) * (kMaxSample + 1) * sizeof(U);
-  s.small_smem = (size_t)kSmallT * (sizeof(U) + (PAY ? 6 : 0));
+  s.small_smem = (size_t)kSmallT * (sizeof(U) + (PAY ? 8 : 0));
   return s;
 }
 

@@ -84,6 +84,7 @@ struct StageMeta {
 
 #include "tsq_partition.cuh"
 #include "tsq_schedule.cuh"
+#include "tsq_small.cuh"
 
 namespace tsq {
 
@@ -142,79 +143,6 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
 // memory (records sort (key, local index) pairs so equal keys keep distinct
 // payloads; padding sorts last).  Output always lands in buffer 0.
 
-template <class C, bool PAY>
-__global__ void __launch_bounds__(kThreads) small_sort_kernel(const Params *__restrict__ P) {
-  typedef typename C::U U;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  U *s_k = reinterpret_cast<U *>(smem_raw);
-  uint32_t *s_p = reinterpret_cast<uint32_t *>(s_k + kSmallT);
-  uint16_t *s_i = reinterpret_cast<uint16_t *>(s_p + (PAY ? kSmallT : 0));
-  __shared__ uint32_t s_ticket;
-  Ctl *ctl = P->ctl;
-  const uint32_t count = ctl->small_count < P->small_cap ? ctl->small_count : P->small_cap;
-  U *dst = reinterpret_cast<U *>(P->keys[0]);
-  const bool dst_raw = P->raw[0] != 0;
-  for (;;) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&ctl->small_ticket, 1u);
-    __syncthreads();
-    const uint32_t t = s_ticket;
-    __syncthreads();
-    if (t >= count) break;
-    const SmallSeg sm = P->smalls[t];
-    const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]);
-    const bool raw = P->raw[sm.buf] != 0;
-    const int len = sm.len;
-    int P2 = 1;
-    while (P2 < len) P2 <<= 1;
-    for (int i = threadIdx.x; i < P2; i += kThreads) {
-      U v = KeyMax<U>::v;
-      if (i < len) {
-        v = src[sm.begin + i];
-        if (raw) v = C::enc(v);
-        if (PAY) s_p[i] = P->pay[sm.buf][sm.begin + i];
-      }
-      s_k[i] = v;
-      if (PAY) s_i[i] = (uint16_t)i;
-    }
-    __syncthreads();
-    for (int kk = 2; kk <= P2; kk <<= 1) {
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < (P2 >> 1); i += kThreads) {
-          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-          const int hi = lo + j;
-          const bool up = (lo & kk) == 0;
-          const U a = s_k[lo], b = s_k[hi];
-          if (PAY) {
-            const uint16_t ia = s_i[lo], ib = s_i[hi];
-            const bool gt = (a > b) || (a == b && ia > ib);
-            if (gt == up) {
-              s_k[lo] = b; s_k[hi] = a;
-              s_i[lo] = ib; s_i[hi] = ia;
-            }
-          } else {
-            if ((a > b) == up) {
-              s_k[lo] = b;
-              s_k[hi] = a;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (int i = threadIdx.x; i < len; i += kThreads) {
-      U v = s_k[i];
-      if (dst_raw) v = C::dec(v);
-      dst[sm.begin + i] = v;
-      if (PAY) P->pay[0][sm.begin + i] = s_p[s_i[i]];
-    }
-    if (threadIdx.x == 0) {
-      atomicAdd(&ctl->small_elements, (u64)len);
-      atomicAdd(&ctl->bytes_small, 2ull * (u64)len * (sizeof(U) + (PAY ? 4 : 0)));
-      atomicAdd(&ctl->writes0, (u64)len);
-    }
-    __syncthreads();
-  }
-}
 
 // Retire finished runs into buffer 0, chunk by chunk.
 template <class C, bool PAY>
