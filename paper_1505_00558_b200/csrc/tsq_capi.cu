@@ -172,10 +172,11 @@ int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem, int block = k
 tsq_status prepare_small_smem(const KernelSet &ks) {
   const void *fns[3] = {ks.part, ks.sched, ks.small};
   const size_t sm[3] = {ks.part_smem, ks.sched_smem, ks.small_smem};
+  // always opt in: dynamic + static shared memory may cross 48 KB even when
+  // the dynamic part alone does not
   for (int i = 0; i < 3; ++i)
-    if (sm[i] > 48 * 1024)
-      TSQ_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sm[i]));
+    TSQ_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm[i]));
   return TSQ_OK;
 }
 
