@@ -38,7 +38,9 @@ KernelSet make_set() {
   s.tile = Geo<C, PAY>::TILE;
   s.part_smem = Geo<C, PAY>::SMEM;
   s.sched_smem = (size_t)(kThreads / 32) * (kMaxSample + 1) * sizeof(U);
-  s.small_smem = (size_t)kSmallT * (sizeof(U) + (PAY ? 8 : 0));
+  // keys + indices in padded rows of 17, staged payloads (see tsq_small.cuh)
+  s.small_smem = (size_t)kThreads * (kSmallT / kThreads + 1) * (sizeof(U) + (PAY ? 4 : 0)) +
+                 (PAY ? (size_t)kSmallT * 4 : 0);
   return s;
 }
 

@@ -3,17 +3,21 @@
 // insertion_threshold keys in the reference (smallsort.py:12-47,
 // core.py:1652-1658), done as a bitonic sorting network.
 //
-// One CTA (256 threads) per segment, the segment padded to N = 256 * E keys
-// (E = 1 .. 16 per thread) with +max sentinels.  Keys live in registers in
-// blocked order (thread t holds elements t*E .. t*E+E-1), so the stages of
-// the network map to three exchange mechanisms:
-//   j <  E        both keys in the same thread's registers (IMNMX)
-//   j <  32 E     partner thread in the same warp (__shfl_xor_sync)
-//   j >= 32 E     partner thread in another warp: one shared-memory round
-//                 trip in register-major order (conflict-free)
-// Records sort (key, local index) pairs so equal keys keep their own
-// payloads and sentinels sort after every real key; payloads are gathered
-// by index at the end.  Output always lands in buffer 0.
+// One CTA (256 threads) per segment, padded to N = 256 * E keys (E = 1 .. 16
+// per thread) with +max sentinels.  Keys live in registers in blocked order
+// (thread t holds elements t*E .. t*E+E-1).  The network is the all-ascending
+// bitonic formulation: merge k starts with a "flip" stage (i against
+// i ^ (k-1)) followed by half-cleaners (i against i ^ j), and every
+// comparator puts the minimum at the lower index -- no direction logic, one
+// min/max pair per comparator.  Stages exchange data three ways:
+//   stride <  E      both keys in the thread's registers
+//   stride <  32 E   partner thread in the same warp (__shfl_xor_sync)
+//   stride >= 32 E   partner in another warp: one shared-memory round trip
+//                    in register-major order (conflict-free)
+// Global I/O is staged through shared memory (padded rows) so it coalesces.
+// Records sort (key, local index) pairs so equal keys keep their own payloads
+// and sentinels sort after every real key; payloads are gathered by index.
+// Output always lands in buffer 0.
 #pragma once
 
 namespace tsq {
@@ -24,23 +28,41 @@ struct SortItem {
   uint32_t i;  // local index (records only)
 };
 
-// "a sorts before b"
 template <typename U, bool PAY>
 __device__ __forceinline__ bool item_less(const SortItem<U, PAY> &a, const SortItem<U, PAY> &b) {
   if (PAY) return a.k < b.k || (a.k == b.k && a.i < b.i);
   return a.k < b.k;
 }
 
-// keep the smaller (keep_min) or larger of (x, y) in x
+// comparator: a <- min, b <- max
+template <typename U, bool PAY>
+__device__ __forceinline__ void cmpx(SortItem<U, PAY> &a, SortItem<U, PAY> &b) {
+  if (PAY) {
+    const bool sw = item_less<U, PAY>(b, a);
+    const SortItem<U, PAY> x = a;
+    a.k = sw ? b.k : a.k;
+    a.i = sw ? b.i : a.i;
+    b.k = sw ? x.k : b.k;
+    b.i = sw ? x.i : b.i;
+  } else {
+    const U x = a.k, y = b.k;
+    a.k = x < y ? x : y;
+    b.k = x < y ? y : x;
+  }
+}
+
+// x <- min(x, y) if keep_min else max(x, y)
 template <typename U, bool PAY>
 __device__ __forceinline__ void keep(SortItem<U, PAY> &x, const SortItem<U, PAY> &y,
                                      bool keep_min) {
-  const bool take = item_less<U, PAY>(y, x) == keep_min;
   if (PAY) {
+    const bool take = item_less<U, PAY>(y, x) == keep_min;
     x.k = take ? y.k : x.k;
     x.i = take ? y.i : x.i;
   } else {
-    x.k = take ? y.k : x.k;
+    const U mn = x.k < y.k ? x.k : y.k;
+    const U mx = x.k < y.k ? y.k : x.k;
+    x.k = keep_min ? mn : mx;
   }
 }
 
@@ -55,70 +77,88 @@ __device__ __forceinline__ u64 shfl_xor_u<u64>(u64 v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
 }
 
+// Exchange with thread tid ^ m: y[r] = partner's v[rev ? E-1-r : r].
+template <typename U, bool PAY, int E>
+__device__ __forceinline__ void exchange(const SortItem<U, PAY> (&v)[E], SortItem<U, PAY> (&y)[E],
+                                         int m, bool rev, U *xk, uint32_t *xi) {
+  const int tid = threadIdx.x;
+  if (m < 32) {
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const SortItem<U, PAY> &s = rev ? v[E - 1 - r] : v[r];
+      y[r].k = shfl_xor_u<U>(s.k, m);
+      if (PAY) y[r].i = __shfl_xor_sync(0xffffffffu, s.i, m);
+    }
+  } else {
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      xk[r * kThreads + tid] = v[r].k;
+      if (PAY) xi[r * kThreads + tid] = v[r].i;
+    }
+    __syncthreads();
+    const int p = tid ^ m;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int rr = rev ? E - 1 - r : r;
+      y[r].k = xk[rr * kThreads + p];
+      if (PAY) y[r].i = xi[rr * kThreads + p];
+    }
+  }
+}
+
+// in-thread half-cleaners with strides E/2 .. 1 (compile-time indices)
+template <typename U, bool PAY, int E>
+__device__ __forceinline__ void half_clean_regs(SortItem<U, PAY> (&v)[E]) {
+#pragma unroll
+  for (int j = E / 2; j >= 1; j >>= 1) {
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+      if (!(r & j)) cmpx<U, PAY>(v[r], v[r | j]);
+  }
+}
+
 // Bitonic sort of N = 256 * E items held as v[E] per thread (blocked).
-// xk / xi: shared scratch of >= N keys / indices for cross-warp stages.
 template <typename U, bool PAY, int E>
 __device__ __forceinline__ void block_bitonic(SortItem<U, PAY> (&v)[E], U *xk, uint32_t *xi) {
   constexpr int N = kThreads * E;
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  // merge size k and cross-thread strides are runtime loops (small code);
-  // in-thread strides are unrolled so register indices stay compile-time
-#pragma unroll 1
-  for (int k = 2; k <= N; k <<= 1) {
-#pragma unroll 1
-    for (int j = k >> 1; j >= E; j >>= 1) {
-      if (j < 32 * E) {
-        // partner thread tid ^ (j / E) in the same warp, same register
-        const int m = j / E;
-        const bool lower = (lane & m) == 0;
+  // merges of size 2 .. E: entirely inside each thread
 #pragma unroll
-        for (int r = 0; r < E; ++r) {
-          const int i = tid * E + r;
-          const bool up = (i & k) == 0;
-          SortItem<U, PAY> y;
-          y.k = shfl_xor_u<U>(v[r].k, m);
-          if (PAY) y.i = __shfl_xor_sync(0xffffffffu, v[r].i, m);
-          keep<U, PAY>(v[r], y, lower == up);
-        }
-      } else {
-        // partner thread tid ^ (j / E) in another warp: register-major
-        // exchange through shared memory (lanes touch consecutive words)
-        const int m = j / E;
-        const bool lower = (tid & m) == 0;
-        __syncthreads();
+  for (int k = 2; k <= E; k <<= 1) {
 #pragma unroll
-        for (int r = 0; r < E; ++r) {
-          xk[r * kThreads + tid] = v[r].k;
-          if (PAY) xi[r * kThreads + tid] = v[r].i;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          const int i = tid * E + r;
-          const bool up = (i & k) == 0;
-          SortItem<U, PAY> y;
-          y.k = xk[r * kThreads + (tid ^ m)];
-          if (PAY) y.i = xi[r * kThreads + (tid ^ m)];
-          keep<U, PAY>(v[r], y, lower == up);
-        }
-      }
+    for (int r = 0; r < E; ++r) {
+      const int p = r ^ (k - 1);
+      if (r < p) cmpx<U, PAY>(v[r], v[p]);
     }
-    // both partners in this thread: strides E/2 .. 1 (those below k)
 #pragma unroll
-    for (int j = E / 2; j >= 1; j >>= 1) {
-      if (j >= k) continue;
+    for (int j = k >> 2; j >= 1; j >>= 1) {
 #pragma unroll
-      for (int r = 0; r < E; ++r) {
-        if (r & j) continue;
-        const int i = tid * E + r;
-        const bool up = (i & k) == 0;
-        SortItem<U, PAY> a = v[r], b = v[r | j];
-        const bool sw = item_less<U, PAY>(b, a) == up;
-        v[r] = sw ? b : a;
-        v[r | j] = sw ? a : b;
-      }
+      for (int r = 0; r < E; ++r)
+        if (!(r & j)) cmpx<U, PAY>(v[r], v[r | j]);
     }
+  }
+  // merges of size 2E .. N: cross-thread strides first, then in registers
+#pragma unroll 1
+  for (int k = 2 * E; k <= N; k <<= 1) {
+    SortItem<U, PAY> y[E];
+    {
+      // flip: element (tid, r) against (tid ^ (k/E - 1), E-1-r)
+      const int m = k / E - 1;
+      const bool lower = (tid & (k / (2 * E))) == 0;
+      exchange<U, PAY, E>(v, y, m, true, xk, xi);
+#pragma unroll
+      for (int r = 0; r < E; ++r) keep<U, PAY>(v[r], y[r], lower);
+    }
+#pragma unroll 1
+    for (int j = k >> 2; j >= E; j >>= 1) {
+      const int m = j / E;
+      const bool lower = (tid & m) == 0;
+      exchange<U, PAY, E>(v, y, m, false, xk, xi);
+#pragma unroll
+      for (int r = 0; r < E; ++r) keep<U, PAY>(v[r], y[r], lower);
+    }
+    half_clean_regs<U, PAY, E>(v);
   }
 }
 
@@ -127,41 +167,52 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
                                                unsigned char *smem) {
   typedef typename C::U U;
   constexpr int N = kThreads * E;
+  constexpr int ROW = E + 1;  // padded row per thread for blocked access
+  // smem: keys [kThreads * ROW] | indices [kThreads * ROW] | payloads [N]
   U *xk = reinterpret_cast<U *>(smem);
-  uint32_t *xi = reinterpret_cast<uint32_t *>(xk + N);
-  uint32_t *sp = xi + (PAY ? N : 0);  // staged payloads (records)
+  uint32_t *xi = reinterpret_cast<uint32_t *>(xk + kThreads * ROW);
+  uint32_t *sp = xi + (PAY ? kThreads * ROW : 0);
   const int tid = threadIdx.x;
   const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
   const bool raw = P->raw[sm.buf] != 0;
   const int len = sm.len;
-  SortItem<U, PAY> v[E];
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int i = tid * E + r;
+  // coalesced load into padded rows: element i -> row i / E, column i % E
+  for (int i = tid; i < N; i += kThreads) {
     U x = KeyMax<U>::v;
     if (i < len) {
       x = src[i];
       if (raw) x = C::enc(x);
     }
-    v[r].k = x;
-    v[r].i = (uint32_t)i;
+    xk[(i / E) * ROW + (i % E)] = x;
   }
   if (PAY) {
     const uint32_t *ps = P->pay[sm.buf] + sm.begin;
     for (int i = tid; i < len; i += kThreads) sp[i] = ps[i];
   }
+  __syncthreads();
+  SortItem<U, PAY> v[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    v[r].k = xk[tid * ROW + r];
+    v[r].i = (uint32_t)(tid * E + r);
+  }
   block_bitonic<U, PAY, E>(v, xk, xi);
-  __syncthreads();  // every key was loaded before any is stored (in place)
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < E; ++r) xk[tid * ROW + r] = v[r].k;
+  if (PAY) {
+    __syncthreads();  // xi (the exchange scratch) becomes the index row buffer
+#pragma unroll
+    for (int r = 0; r < E; ++r) xi[tid * ROW + r] = v[r].i;
+  }
+  __syncthreads();
   U *dst = reinterpret_cast<U *>(P->keys[0]) + sm.begin;
   const bool dst_raw = P->raw[0] != 0;
   uint32_t *pd = PAY ? P->pay[0] + sm.begin : nullptr;
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int i = tid * E + r;
-    if (i < len) {
-      dst[i] = dst_raw ? C::dec(v[r].k) : v[r].k;
-      if (PAY) pd[i] = sp[v[r].i];
-    }
+  for (int i = tid; i < len; i += kThreads) {
+    const U x = xk[(i / E) * ROW + (i % E)];
+    dst[i] = dst_raw ? C::dec(x) : x;
+    if (PAY) pd[i] = sp[xi[(i / E) * ROW + (i % E)]];
   }
 }
 
