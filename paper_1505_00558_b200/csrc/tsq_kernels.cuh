@@ -83,8 +83,8 @@ struct StageMeta {
 }  // namespace tsq
 
 #include "tsq_partition.cuh"
-#include "tsq_schedule.cuh"
 #include "tsq_small.cuh"
+#include "tsq_schedule.cuh"
 
 namespace tsq {
 

@@ -6,10 +6,13 @@
 // For every segment of the level just partitioned: retire the == p block
 // (never compared again), then queue each child -- the < part and the > part
 // -- either for the on-chip sort (<= small_t keys) or for the next level
-// with its pivot sampled now (select_pivot's role, pivot.py:205-248).  A
-// group of threads owns one segment: a whole CTA while segments are large
-// (few segments, 1023-key samples), one warp per segment once they are small
-// (thousands of segments, 31..255-key samples).
+// with its pivot sampled now (select_pivot's role, pivot.py:205-248).
+//   few, large segments   one CTA per segment, 1023-key samples sorted by a
+//                         register bitonic network across the CTA
+//   many, small segments  one warp per segment, <= 255-key samples sorted in
+//                         the warp's registers; the queue slots of all of a
+//                         CTA's segments are claimed with one atomic per
+//                         queue per round (the queues are single hot words)
 #pragma once
 
 namespace tsq {
@@ -20,88 +23,10 @@ enum SchedStat {
   ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_COUNT
 };
 
-// A cooperating group: one warp, or the whole CTA.
-template <bool CTA>
-struct Group {
-  static constexpr int SIZE = CTA ? kThreads : 32;
-  static __device__ __forceinline__ int rank() { return CTA ? (int)threadIdx.x : (int)(threadIdx.x & 31); }
-  static __device__ __forceinline__ void sync() {
-    if (CTA) __syncthreads(); else __syncwarp();
-  }
-};
-
-// Queue a segment for the next level: the leader claims the slot and its
-// tile range with one packed atomic, the group fills the tile map.
-template <class C, bool PAY, bool CTA>
-__device__ void group_append_level(const Params *P, int nxt, long long begin, long long end,
-                                   uint32_t buf, u64 pivot, uint32_t kind, uint32_t depth,
-                                   uint32_t noverify, volatile uint32_t *bc) {
-  typedef Group<CTA> G;
-  const long long T = Geo<C, PAY>::TILE;
-  const uint32_t ntiles = (uint32_t)((end - 1) / T - begin / T + 1);
-  if (G::rank() == 0) {
-    Ctl *ctl = P->ctl;
-    const u64 old = atomicAdd(&ctl->next_packed, (1ull << 32) | ntiles);
-    uint32_t slot = (uint32_t)(old >> 32);
-    const uint32_t tbase = (uint32_t)old;
-    if (slot < P->seg_cap && (u64)tbase + ntiles <= P->tile_cap) {
-      Seg s;
-      s.begin = begin; s.end = end; s.pivot = pivot;
-      s.tile_base = tbase; s.ntiles = ntiles;
-      s.buf = buf; s.kind = kind; s.depth = depth; s.noverify = noverify;
-      s.done = 0; s.fail = 0;
-      P->segs[nxt][slot] = s;
-    } else {
-      atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-      slot = kDone;
-    }
-    bc[0] = slot;
-    bc[1] = tbase;
-  }
-  G::sync();
-  const uint32_t slot = bc[0], tbase = bc[1];
-  if (slot != kDone) {
-    uint32_t *tm = P->tilemap[nxt] + tbase;
-    for (uint32_t i = G::rank(); i < ntiles; i += G::SIZE) tm[i] = slot;
-  }
-  G::sync();
-}
-
-template <bool CTA>
-__device__ void group_append_run(const Params *P, uint32_t kind, long long begin, long long len,
-                                 uint32_t buf, u64 pivot, long long src, volatile uint32_t *bc) {
-  typedef Group<CTA> G;
-  uint32_t nchunks;
-  if (kind == RUN_REVERSED && buf == 0)
-    nchunks = (uint32_t)(((len >> 1) + kRunChunk - 1) / kRunChunk);
-  else
-    nchunks = (uint32_t)((len + kRunChunk - 1) / kRunChunk);
-  if (nchunks == 0) return;
-  if (G::rank() == 0) {
-    Ctl *ctl = P->ctl;
-    const u64 old = atomicAdd(&ctl->run_packed, (1ull << 32) | nchunks);
-    uint32_t slot = (uint32_t)(old >> 32);
-    const uint32_t cbase = (uint32_t)old;
-    if (slot < P->run_cap && (u64)cbase + nchunks <= P->chunk_cap) {
-      Run r;
-      r.begin = begin; r.len = len; r.pivot = pivot; r.src = src;
-      r.kind = kind; r.buf = buf; r.chunk_base = cbase; r.nchunks = nchunks;
-      P->runs[slot] = r;
-    } else {
-      atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-      slot = kDone;
-    }
-    bc[0] = slot;
-    bc[1] = cbase;
-  }
-  G::sync();
-  const uint32_t slot = bc[0], cbase = bc[1];
-  if (slot != kDone) {
-    uint32_t *cm = P->chunkmap + cbase;
-    for (uint32_t i = G::rank(); i < nchunks; i += G::SIZE) cm[i] = slot;
-  }
-  G::sync();
-}
+constexpr int kWarpSampleMax = 255;   // warp-mode sample cap (8 per lane)
+// Segments of at least this many keys (on average) are scheduled by a whole
+// CTA each; below it one warp per segment.
+constexpr long long kCtaScheduleMin = 1ll << 17;
 
 __device__ __forceinline__ void append_small(const Params *P, long long begin, long long len,
                                              uint32_t buf) {
@@ -116,121 +41,233 @@ __device__ __forceinline__ void append_small(const Params *P, long long begin, l
   }
 }
 
-// ---- group pivot sampling (select_pivot analogue, pivot.py:205-248) --------
-// Median of S = sample_count(len) strided samples; the first, middle and
-// last positions are fixed anchors and interior positions shift by the
-// MitigationRng jitter (dran, pivot.py:223-237).  *flag gets the order flag
-// of the samples in position order (+1 nondecreasing, -1 nonincreasing).
-// `s` is the group's scratch of kMaxSample + 1 keys.
-template <class C, bool CTA>
-__device__ typename C::U group_select_pivot(const typename C::U *data, bool encoded_src,
-                                            long long begin, long long len, double dran,
-                                            int mitigation, typename C::U *s, int *flag,
-                                            volatile uint32_t *bc) {
+template <class C, bool PAY>
+__device__ __forceinline__ uint32_t tiles_of(long long begin, long long end) {
+  const long long T = Geo<C, PAY>::TILE;
+  return (uint32_t)((end - 1) / T - begin / T + 1);
+}
+
+__device__ __forceinline__ uint32_t chunks_of(uint32_t kind, long long len, uint32_t buf) {
+  if (kind == RUN_REVERSED && buf == 0) return (uint32_t)(((len >> 1) + kRunChunk - 1) / kRunChunk);
+  return (uint32_t)((len + kRunChunk - 1) / kRunChunk);
+}
+
+// ---- sample sorting networks (all-ascending bitonic, as in tsq_small.cuh) --
+
+// warp: 32 * Q keys, lane l holds l*Q .. l*Q+Q-1
+template <typename U, int Q>
+__device__ __forceinline__ void warp_bitonic(U (&v)[Q]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32 * Q; k <<= 1) {
+    if (k <= Q) {
+#pragma unroll
+      for (int r = 0; r < Q; ++r) {
+        const int p = r ^ (k - 1);
+        if (r < p) { const U a = v[r], b = v[p]; v[r] = a < b ? a : b; v[p] = a < b ? b : a; }
+      }
+    } else {
+      const int m = k / Q - 1;
+      const bool lower = (lane & (k / (2 * Q))) == 0;
+      U y[Q];
+#pragma unroll
+      for (int r = 0; r < Q; ++r) y[r] = __shfl_xor_sync(0xffffffffu, v[Q - 1 - r], m);
+#pragma unroll
+      for (int r = 0; r < Q; ++r) {
+        const U mn = v[r] < y[r] ? v[r] : y[r], mx = v[r] < y[r] ? y[r] : v[r];
+        v[r] = lower ? mn : mx;
+      }
+    }
+#pragma unroll
+    for (int j = k >> 2; j >= 1; j >>= 1) {
+      if (j >= Q) {
+        const int m = j / Q;
+        const bool lower = (lane & m) == 0;
+#pragma unroll
+        for (int r = 0; r < Q; ++r) {
+          const U y = __shfl_xor_sync(0xffffffffu, v[r], m);
+          const U mn = v[r] < y ? v[r] : y, mx = v[r] < y ? y : v[r];
+          v[r] = lower ? mn : mx;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < Q; ++r)
+          if (!(r & j)) { const U a = v[r], b = v[r | j]; v[r] = a < b ? a : b; v[r | j] = a < b ? b : a; }
+      }
+    }
+  }
+}
+
+// Load the S strided samples of [begin, begin+len) in position order into
+// v (blocked, padded with +max to `slots` entries).  The first, middle and
+// last positions are fixed anchors; interior positions shift by the
+// MitigationRng jitter (dran, pivot.py:223-237).
+template <class C, int Q>
+__device__ __forceinline__ void load_samples(const typename C::U *data, bool encoded_src,
+                                             long long begin, long long len, int S, double dran,
+                                             int mitigation, int owner, typename C::U (&v)[Q]) {
   typedef typename C::U U;
-  typedef Group<CTA> G;
-  constexpr int Q = (kMaxSample + 1) / G::SIZE;
-  const int r = G::rank();
-  const int S = sample_count(len);
-  const int P2 = S + 1;
   const int midi = S >> 1;
   const long long span = len - 1;
   long long shift = 0;
-  if (mitigation) {
-    const double stride = (double)span / (double)(S - 1);
-    shift = (long long)floor((dran - 1.0) * stride * 0.5);
-  }
   const double step = (double)span / (double)(S - 1);
-  // all of a thread's sample loads are issued before any is consumed
-  U vals[Q];
+  if (mitigation) shift = (long long)floor((dran - 1.0) * step * 0.5);
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
-    const int i = r + G::SIZE * q;
-    vals[q] = KeyMax<U>::v;
+    const int i = owner * Q + q;
+    v[q] = KeyMax<U>::v;
     if (i < S) {
       long long pos = (i == S - 1) ? begin + span : begin + (long long)((double)i * step);
       if (i != 0 && i != midi && i != S - 1) {
         pos += shift;
         pos = pos < begin ? begin : (pos > begin + span ? begin + span : pos);
       }
-      vals[q] = ldcg(data + pos);
+      const U x = ldcg(data + pos);
+      v[q] = encoded_src ? x : C::enc(x);
     }
   }
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    const int i = r + G::SIZE * q;
-    if (i < P2) s[i] = (i < S && !encoded_src) ? C::enc(vals[q]) : vals[q];
-  }
-  G::sync();
+}
+
+// order flag of the samples in position order (+1 nondecreasing, -1
+// nonincreasing, 0) for a warp holding them blocked
+template <typename U, int Q>
+__device__ __forceinline__ int warp_order_flag(const U (&v)[Q], int S) {
+  const int lane = threadIdx.x & 31;
   bool asc = true, desc = true;
-  for (int i = r; i < S - 1; i += G::SIZE) {
-    const U a = s[i], b = s[i + 1];
-    asc &= (a <= b);
-    desc &= (a >= b);
-  }
-  if (CTA) {
-    asc = __syncthreads_and(asc);
-    desc = __syncthreads_and(desc);
-  } else {
-    asc = __all_sync(0xffffffffu, asc);
-    desc = __all_sync(0xffffffffu, desc);
-  }
-  for (int k = 2; k <= P2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = r; i < (P2 >> 1); i += G::SIZE) {
-        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-        const int hi = lo + j;
-        const bool up = (lo & k) == 0;
-        const U a = s[lo], b = s[hi];
-        if ((a > b) == up) {
-          s[lo] = b;
-          s[hi] = a;
-        }
-      }
-      G::sync();
+#pragma unroll
+  for (int q = 0; q + 1 < Q; ++q) {
+    if (lane * Q + q + 1 < S) {
+      asc &= v[q] <= v[q + 1];
+      desc &= v[q] >= v[q + 1];
     }
   }
+  const U nxt = __shfl_down_sync(0xffffffffu, v[0], 1);
+  if (lane < 31 && (lane + 1) * Q < S) {
+    asc &= v[Q - 1] <= nxt;
+    desc &= v[Q - 1] >= nxt;
+  }
+  asc = __all_sync(0xffffffffu, asc);
+  desc = __all_sync(0xffffffffu, desc);
+  return asc ? 1 : (desc ? -1 : 0);
+}
+
+template <typename U, int Q>
+__device__ __forceinline__ U warp_pick(const U (&v)[Q], int idx) {
+  U x = v[0];
+#pragma unroll
+  for (int q = 1; q < Q; ++q)
+    if ((idx % Q) == q) x = v[q];
+  return __shfl_sync(0xffffffffu, x, idx / Q);
+}
+
+// warp pivot sampling: S <= kWarpSampleMax
+template <class C, int Q>
+__device__ __forceinline__ typename C::U warp_pivot_q(const typename C::U *data, bool enc_src,
+                                                      long long begin, long long len, int S,
+                                                      double dran, int mitigation, int *flag) {
+  typedef typename C::U U;
+  U v[Q];
+  load_samples<C, Q>(data, enc_src, begin, len, S, dran, mitigation, threadIdx.x & 31, v);
+  *flag = warp_order_flag<U, Q>(v, S);
+  warp_bitonic<U, Q>(v);
+  return warp_pick<U, Q>(v, S >> 1);
+}
+
+template <class C>
+__device__ typename C::U warp_select_pivot(const typename C::U *data, bool enc_src,
+                                           long long begin, long long len, double dran,
+                                           int mitigation, int *flag) {
+  int S = sample_count(len);
+  if (S > kWarpSampleMax) S = kWarpSampleMax;
+  if (S <= 32) return warp_pivot_q<C, 1>(data, enc_src, begin, len, S, dran, mitigation, flag);
+  if (S <= 64) return warp_pivot_q<C, 2>(data, enc_src, begin, len, S, dran, mitigation, flag);
+  if (S <= 128) return warp_pivot_q<C, 4>(data, enc_src, begin, len, S, dran, mitigation, flag);
+  return warp_pivot_q<C, 8>(data, enc_src, begin, len, S, dran, mitigation, flag);
+}
+
+// CTA pivot sampling: S <= 1023 samples, 4 per thread, register bitonic with
+// shuffle and shared-memory stages (block_bitonic from tsq_small.cuh)
+template <class C>
+__device__ typename C::U cta_select_pivot_fast(const typename C::U *data, bool enc_src,
+                                               long long begin, long long len, double dran,
+                                               int mitigation, typename C::U *xk,
+                                               volatile uint32_t *bc, int *flag) {
+  typedef typename C::U U;
+  constexpr int Q = 4;  // 256 * 4 = 1024 slots
+  const int S = sample_count(len);
+  const int tid = threadIdx.x;
+  U raw[Q];
+  load_samples<C, Q>(data, enc_src, begin, len, S, dran, mitigation, tid, raw);
+  // order flag over position order
+  bool asc = true, desc = true;
+#pragma unroll
+  for (int q = 0; q + 1 < Q; ++q)
+    if (tid * Q + q + 1 < S) {
+      asc &= raw[q] <= raw[q + 1];
+      desc &= raw[q] >= raw[q + 1];
+    }
+  xk[tid] = raw[0];
+  __syncthreads();
+  if (tid < kThreads - 1 && (tid + 1) * Q < S) {
+    asc &= raw[Q - 1] <= xk[tid + 1];
+    desc &= raw[Q - 1] >= xk[tid + 1];
+  }
+  asc = __syncthreads_and(asc);
+  desc = __syncthreads_and(desc);
   *flag = asc ? 1 : (desc ? -1 : 0);
-  const U piv = s[midi];
-  G::sync();
+  SortItem<U, false> v[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) v[q].k = raw[q];
+  block_bitonic<U, false, Q>(v, xk, nullptr);
+  const int midi = S >> 1;
+  __syncthreads();
+  if (tid == midi / Q) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (q == midi % Q) xk[0] = v[q].k;
+  }
+  __syncthreads();
+  const U piv = xk[0];
+  __syncthreads();
+  (void)bc;
   return piv;
 }
 
 // ---------------------------------------------------------------------------
+// Segment head: statistics, verification outcome, == p retirement.  Returns
+// the child layout in *lt / *gt, or false when the segment produced no
+// children to schedule (verified run, failed verification re-queued, single
+// stage).  Executed by a whole group; queue appends here are rare (runs).
 
 template <class C, bool PAY, bool CTA>
-__device__ void schedule_segment(const Params *P, int cur, int nxt, uint32_t sid,
-                                 typename C::U *scratch, u64 *st, volatile uint32_t *bc) {
+__device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u64 *st,
+                             long long *lt_out, long long *gt_out, uint32_t *requeue) {
   typedef typename C::U U;
-  typedef Group<CTA> G;
-  const int r = G::rank();
+  const int r = CTA ? (int)threadIdx.x : (int)(threadIdx.x & 31);
+  const int gsize = CTA ? kThreads : 32;
   const bool leader = r == 0;
   Ctl *ctl = P->ctl;
-  const Seg sg = P->segs[cur][sid];
   const long long len = sg.end - sg.begin;
   const int kb = (int)sizeof(U);
+  *requeue = 0;
   if (sg.kind != KIND_PARTITION) {
-    const bool failed = sg.fail != 0;
-    if (!failed) {
+    if (sg.fail == 0) {
       const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
-      const bool moves = !(rk == RUN_SORTED && sg.buf == 0);
       if (leader) {
         atomicAdd(&st[ST_STAGES], 1ull);
         atomicAdd(&st[rk == RUN_SORTED ? ST_SORTED : ST_REVERSED], 1ull);
         atomicMax(&st[ST_DEPTH], (u64)sg.depth);
         atomicAdd(&st[ST_BYTES_PART], (u64)len * kb);  // the verify read
-        if (moves) {
+        if (!(rk == RUN_SORTED && sg.buf == 0)) {
           atomicAdd(&st[ST_BYTES_RETIRE], 2ull * (u64)len * (u64)(kb + (PAY ? 4 : 0)));
           atomicAdd(&st[ST_W0], (u64)len);
         }
       }
-      if (moves) group_append_run<CTA>(P, rk, sg.begin, len, sg.buf, 0ull, sg.begin, bc);
     } else {
       if (leader) atomicAdd(&st[ST_FALLBACK], 1ull);
-      group_append_level<C, PAY, CTA>(P, nxt, sg.begin, sg.end, sg.buf, sg.pivot,
-                                      KIND_PARTITION, sg.depth, 1, bc);
+      *requeue = 1;
     }
-    return;
+    return false;
   }
   const u64 inc = P->lookback[cur][sg.tile_base + sg.ntiles - 1];
   const long long lt = (long long)((inc >> 31) & 0x7fffffffull);
@@ -256,68 +293,342 @@ __device__ void schedule_segment(const Params *P, int cur, int nxt, uint32_t sid
       ctl->stage_gt = (u64)gt;
     }
   }
-  if (eq > 0) {
-    if (PAY) {
-      // Records: the == p payloads sit at side_pay[begin ...], a range the
-      // children reuse at the next level, so they move to their final place
-      // now (nothing else touches [begin+lt, end-gt) of buffer 0).
-      const uint32_t *side = P->side_pay + sg.begin;
-      uint32_t *p0 = P->pay[0] + sg.begin + lt;
-      U *k0 = reinterpret_cast<U *>(P->keys[0]) + sg.begin + lt;
-      const U v = P->raw[0] ? C::dec((U)sg.pivot) : (U)sg.pivot;
-      for (long long i = r; i < eq; i += G::SIZE) {
-        p0[i] = side[i];
-        k0[i] = v;
-      }
-    } else {
-      group_append_run<CTA>(P, RUN_EQ, sg.begin + lt, eq, sg.buf, sg.pivot, sg.begin, bc);
+  if (eq > 0 && PAY) {
+    // Records: the == p payloads sit at side_pay[begin ...], a range the
+    // children reuse at the next level, so they move to their final place
+    // now (nothing else touches [begin+lt, end-gt) of buffer 0).
+    const uint32_t *side = P->side_pay + sg.begin;
+    uint32_t *p0 = P->pay[0] + sg.begin + lt;
+    U *k0 = reinterpret_cast<U *>(P->keys[0]) + sg.begin + lt;
+    const U v = P->raw[0] ? C::dec((U)sg.pivot) : (U)sg.pivot;
+    for (long long i = r; i < eq; i += gsize) {
+      p0[i] = side[i];
+      k0[i] = v;
     }
   }
-  if (P->single_stage) return;
+  *lt_out = lt;
+  *gt_out = gt;
+  return !P->single_stage;
+}
+
+// ---------------------------------------------------------------------------
+// Appends aggregated over one round of the CTA's warps.
+
+struct ReqLevel {  // a child queued for the next level
+  long long begin, end;
+  u64 pivot;
+  uint32_t buf, kind, depth, noverify, ntiles, valid;
+};
+struct ReqRun {
+  long long begin, len, src;
+  u64 pivot;
+  uint32_t kind, buf, nchunks, valid;
+};
+struct ReqSmall {
+  long long begin, len;
+  uint32_t buf, valid;
+};
+
+struct RoundShared {
+  ReqLevel lv[kThreads / 32][2];
+  ReqRun run[kThreads / 32];
+  ReqSmall sm[kThreads / 32][2];
+  uint32_t lv_slot0, lv_tile0, run_slot0, run_chunk0, sm_slot0;
+};
+
+template <class C, bool PAY>
+__device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t sid, bool have,
+                                    u64 *st, RoundShared &rs) {
+  typedef typename C::U U;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    rs.lv[warp][0].valid = rs.lv[warp][1].valid = 0;
+    rs.sm[warp][0].valid = rs.sm[warp][1].valid = 0;
+    rs.run[warp].valid = 0;
+  }
+  __syncwarp();
+  if (have) {
+    const Seg sg = P->segs[cur][sid];
+    long long lt = 0, gt = 0;
+    uint32_t requeue = 0;
+    const bool kids = segment_head<C, PAY, false>(P, nxt, sg, cur, st, &lt, &gt, &requeue);
+    const long long len = sg.end - sg.begin;
+    if (lane == 0) {
+      if (sg.kind != KIND_PARTITION) {
+        if (requeue) {
+          ReqLevel &q = rs.lv[warp][0];
+          q.begin = sg.begin; q.end = sg.end; q.pivot = sg.pivot; q.buf = sg.buf;
+          q.kind = KIND_PARTITION; q.depth = sg.depth; q.noverify = 1;
+          q.ntiles = tiles_of<C, PAY>(sg.begin, sg.end); q.valid = 1;
+        } else if (sg.fail == 0) {
+          const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
+          if (!(rk == RUN_SORTED && sg.buf == 0)) {
+            ReqRun &q = rs.run[warp];
+            q.begin = sg.begin; q.len = len; q.src = sg.begin; q.pivot = 0; q.kind = rk;
+            q.buf = sg.buf; q.nchunks = chunks_of(rk, len, sg.buf); q.valid = 1;
+          }
+        }
+      } else {
+        const long long eq = len - lt - gt;
+        if (eq > 0 && !PAY) {
+          ReqRun &q = rs.run[warp];
+          q.begin = sg.begin + lt; q.len = eq; q.src = sg.begin; q.pivot = sg.pivot;
+          q.kind = RUN_EQ; q.buf = sg.buf; q.nchunks = chunks_of(RUN_EQ, eq, sg.buf); q.valid = 1;
+        }
+      }
+    }
+    if (kids) {
+      const uint32_t db = sg.buf ^ 1u;
+      const uint32_t depth = sg.depth + 1;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const long long cb = c == 0 ? sg.begin : sg.end - gt;
+        const long long cl = c == 0 ? lt : gt;
+        if (cl <= 0) continue;
+        if (cl <= P->small_t) {
+          if (lane == 0) {
+            ReqSmall &q = rs.sm[warp][c];
+            q.begin = cb; q.len = cl; q.buf = db; q.valid = 1;
+            atomicMax(&st[ST_DEPTH], (u64)depth);
+          }
+          continue;
+        }
+        if ((int)depth > P->max_depth) {
+          if (lane == 0) atomicOr(&P->ctl->error, (uint32_t)ERR_DEPTH);
+          continue;
+        }
+        int flag = 0;
+        const U piv = warp_select_pivot<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
+                                           cb, cl, P->dran, P->mitigation, &flag);
+        if (lane == 0) {
+          uint32_t kind = KIND_PARTITION;
+          if (P->fast_paths)
+            kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
+          ReqLevel &q = rs.lv[warp][c];
+          q.begin = cb; q.end = cb + cl; q.pivot = (u64)piv; q.buf = db; q.kind = kind;
+          q.depth = depth; q.noverify = 0; q.ntiles = tiles_of<C, PAY>(cb, cb + cl); q.valid = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // one claim per queue for the whole round
+  if (threadIdx.x == 0) {
+    uint32_t nl = 0, nt = 0, nr = 0, nc = 0, ns = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      for (int c = 0; c < 2; ++c) {
+        if (rs.lv[w][c].valid) { ++nl; nt += rs.lv[w][c].ntiles; }
+        if (rs.sm[w][c].valid) ++ns;
+      }
+      if (rs.run[w].valid) { ++nr; nc += rs.run[w].nchunks; }
+    }
+    Ctl *ctl = P->ctl;
+    if (nl) {
+      const u64 old = atomicAdd(&ctl->next_packed, ((u64)nl << 32) | nt);
+      rs.lv_slot0 = (uint32_t)(old >> 32);
+      rs.lv_tile0 = (uint32_t)old;
+      if (rs.lv_slot0 + nl > P->seg_cap || (u64)rs.lv_tile0 + nt > P->tile_cap) {
+        atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+        rs.lv_slot0 = kDone;
+      }
+    }
+    if (nr) {
+      const u64 old = atomicAdd(&ctl->run_packed, ((u64)nr << 32) | nc);
+      rs.run_slot0 = (uint32_t)(old >> 32);
+      rs.run_chunk0 = (uint32_t)old;
+      if (rs.run_slot0 + nr > P->run_cap || (u64)rs.run_chunk0 + nc > P->chunk_cap) {
+        atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+        rs.run_slot0 = kDone;
+      }
+    }
+    if (ns) {
+      rs.sm_slot0 = atomicAdd(&ctl->small_count, ns);
+      if (rs.sm_slot0 + ns > P->small_cap) {
+        atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+        rs.sm_slot0 = kDone;
+      }
+    }
+  }
+  __syncthreads();
+  // each warp writes its records at its offsets
+  uint32_t lslot = rs.lv_slot0, ltile = rs.lv_tile0, rslot = rs.run_slot0;
+  uint32_t rchunk = rs.run_chunk0, sslot = rs.sm_slot0;
+  for (int w = 0; w < warp; ++w) {
+    for (int c = 0; c < 2; ++c) {
+      if (rs.lv[w][c].valid) { ++lslot; ltile += rs.lv[w][c].ntiles; }
+      if (rs.sm[w][c].valid) ++sslot;
+    }
+    if (rs.run[w].valid) { ++rslot; rchunk += rs.run[w].nchunks; }
+  }
+  for (int c = 0; c < 2; ++c) {
+    const ReqLevel &q = rs.lv[warp][c];
+    if (q.valid) {
+      if (rs.lv_slot0 != kDone) {
+        if (lane == 0) {
+          Seg s;
+          s.begin = q.begin; s.end = q.end; s.pivot = q.pivot;
+          s.tile_base = ltile; s.ntiles = q.ntiles;
+          s.buf = q.buf; s.kind = q.kind; s.depth = q.depth; s.noverify = q.noverify;
+          s.done = 0; s.fail = 0;
+          P->segs[nxt][lslot] = s;
+        }
+        uint32_t *tm = P->tilemap[nxt] + ltile;
+        for (uint32_t i = lane; i < q.ntiles; i += 32) tm[i] = lslot;
+      }
+      ++lslot;
+      ltile += q.ntiles;
+    }
+    const ReqSmall &m = rs.sm[warp][c];
+    if (m.valid) {
+      if (rs.sm_slot0 != kDone && lane == 0) {
+        SmallSeg s;
+        s.begin = m.begin; s.len = (int)m.len; s.buf = (int)m.buf;
+        P->smalls[sslot] = s;
+      }
+      ++sslot;
+    }
+  }
+  const ReqRun &q = rs.run[warp];
+  if (q.valid && rs.run_slot0 != kDone) {
+    if (lane == 0) {
+      Run r;
+      r.begin = q.begin; r.len = q.len; r.pivot = q.pivot; r.src = q.src;
+      r.kind = q.kind; r.buf = q.buf; r.chunk_base = rchunk; r.nchunks = q.nchunks;
+      P->runs[rslot] = r;
+    }
+    uint32_t *cm = P->chunkmap + rchunk;
+    for (uint32_t i = lane; i < q.nchunks; i += 32) cm[i] = rslot;
+  }
+  __syncthreads();  // the round's shared requests are consumed
+}
+
+// CTA-wide appends (CTA mode: few segments, no contention to aggregate)
+template <class C, bool PAY>
+__device__ void cta_append_level(const Params *P, int nxt, long long begin, long long end,
+                                 uint32_t buf, u64 pivot, uint32_t kind, uint32_t depth,
+                                 uint32_t noverify, volatile uint32_t *bc) {
+  const uint32_t ntiles = tiles_of<C, PAY>(begin, end);
+  if (threadIdx.x == 0) {
+    Ctl *ctl = P->ctl;
+    const u64 old = atomicAdd(&ctl->next_packed, (1ull << 32) | ntiles);
+    uint32_t slot = (uint32_t)(old >> 32);
+    const uint32_t tbase = (uint32_t)old;
+    if (slot < P->seg_cap && (u64)tbase + ntiles <= P->tile_cap) {
+      Seg s;
+      s.begin = begin; s.end = end; s.pivot = pivot;
+      s.tile_base = tbase; s.ntiles = ntiles;
+      s.buf = buf; s.kind = kind; s.depth = depth; s.noverify = noverify;
+      s.done = 0; s.fail = 0;
+      P->segs[nxt][slot] = s;
+    } else {
+      atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+      slot = kDone;
+    }
+    bc[0] = slot;
+    bc[1] = tbase;
+  }
+  __syncthreads();
+  const uint32_t slot = bc[0], tbase = bc[1];
+  if (slot != kDone) {
+    uint32_t *tm = P->tilemap[nxt] + tbase;
+    for (uint32_t i = threadIdx.x; i < ntiles; i += kThreads) tm[i] = slot;
+  }
+  __syncthreads();
+}
+
+__device__ void cta_append_run(const Params *P, uint32_t kind, long long begin, long long len,
+                               uint32_t buf, u64 pivot, long long src, volatile uint32_t *bc) {
+  const uint32_t nchunks = chunks_of(kind, len, buf);
+  if (nchunks == 0) return;
+  if (threadIdx.x == 0) {
+    Ctl *ctl = P->ctl;
+    const u64 old = atomicAdd(&ctl->run_packed, (1ull << 32) | nchunks);
+    uint32_t slot = (uint32_t)(old >> 32);
+    const uint32_t cbase = (uint32_t)old;
+    if (slot < P->run_cap && (u64)cbase + nchunks <= P->chunk_cap) {
+      Run r;
+      r.begin = begin; r.len = len; r.pivot = pivot; r.src = src;
+      r.kind = kind; r.buf = buf; r.chunk_base = cbase; r.nchunks = nchunks;
+      P->runs[slot] = r;
+    } else {
+      atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+      slot = kDone;
+    }
+    bc[0] = slot;
+    bc[1] = cbase;
+  }
+  __syncthreads();
+  const uint32_t slot = bc[0], cbase = bc[1];
+  if (slot != kDone) {
+    uint32_t *cm = P->chunkmap + cbase;
+    for (uint32_t i = threadIdx.x; i < nchunks; i += kThreads) cm[i] = slot;
+  }
+  __syncthreads();
+}
+
+template <class C, bool PAY>
+__device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t sid,
+                                     typename C::U *xk, u64 *st, volatile uint32_t *bc) {
+  typedef typename C::U U;
+  const Seg sg = P->segs[cur][sid];
+  long long lt = 0, gt = 0;
+  uint32_t requeue = 0;
+  const bool kids = segment_head<C, PAY, true>(P, nxt, sg, cur, st, &lt, &gt, &requeue);
+  __syncthreads();
+  const long long len = sg.end - sg.begin;
+  if (sg.kind != KIND_PARTITION) {
+    if (requeue) {
+      cta_append_level<C, PAY>(P, nxt, sg.begin, sg.end, sg.buf, sg.pivot, KIND_PARTITION,
+                               sg.depth, 1, bc);
+    } else {
+      const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
+      if (!(rk == RUN_SORTED && sg.buf == 0))
+        cta_append_run(P, rk, sg.begin, len, sg.buf, 0ull, sg.begin, bc);
+    }
+    return;
+  }
+  const long long eq = len - lt - gt;
+  if (eq > 0 && !PAY) cta_append_run(P, RUN_EQ, sg.begin + lt, eq, sg.buf, sg.pivot, sg.begin, bc);
+  if (!kids) return;
   const uint32_t db = sg.buf ^ 1u;
   const uint32_t depth = sg.depth + 1;
-#pragma unroll
   for (int c = 0; c < 2; ++c) {
     const long long cb = c == 0 ? sg.begin : sg.end - gt;
     const long long cl = c == 0 ? lt : gt;
     if (cl <= 0) continue;
     if (cl <= P->small_t) {
-      if (leader) {
+      if (threadIdx.x == 0) {
         append_small(P, cb, cl, db);
         atomicMax(&st[ST_DEPTH], (u64)depth);
       }
       continue;
     }
     if ((int)depth > P->max_depth) {
-      if (leader) atomicOr(&ctl->error, (uint32_t)ERR_DEPTH);
+      if (threadIdx.x == 0) atomicOr(&P->ctl->error, (uint32_t)ERR_DEPTH);
       continue;
     }
     int flag = 0;
-    const U piv = group_select_pivot<C, CTA>(reinterpret_cast<const U *>(P->keys[db]),
-                                             !P->raw[db], cb, cl, P->dran, P->mitigation,
-                                             scratch, &flag, bc);
+    const U piv = cta_select_pivot_fast<C>(reinterpret_cast<const U *>(P->keys[db]),
+                                           !P->raw[db], cb, cl, P->dran, P->mitigation, xk, bc,
+                                           &flag);
     uint32_t kind = KIND_PARTITION;
     if (P->fast_paths)
       kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
-    group_append_level<C, PAY, CTA>(P, nxt, cb, cb + cl, db, (u64)piv, kind, depth, 0, bc);
+    cta_append_level<C, PAY>(P, nxt, cb, cb + cl, db, (u64)piv, kind, depth, 0, bc);
   }
 }
-
-// Segments of at least this many keys (on average) are scheduled by a whole
-// CTA each; below it one warp per segment.
-constexpr long long kCtaScheduleMin = 1ll << 17;
 
 template <class C, bool PAY>
 __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__restrict__ P) {
   typedef typename C::U U;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ u64 st[ST_COUNT];
-  __shared__ uint32_t bcast[kThreads / 32][2];
+  __shared__ uint32_t bcast[2];
+  __shared__ RoundShared rs;
   Ctl *ctl = P->ctl;
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u), nxt = cur ^ 1;
   const uint32_t nseg = ctl->cur_nseg;
-  const int warp = threadIdx.x >> 5;
   {
     u64 *lbn = P->lookback[nxt];
     const uint32_t cap = P->tile_cap;
@@ -328,14 +639,15 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
   __syncthreads();
   const long long avg = nseg ? ((long long)ctl->cur_ntiles * Geo<C, PAY>::TILE) / nseg : 0;
   if (avg >= kCtaScheduleMin) {
-    U *scratch = reinterpret_cast<U *>(smem_raw);
+    U *xk = reinterpret_cast<U *>(smem_raw);
     for (uint32_t sid = blockIdx.x; sid < nseg; sid += gridDim.x)
-      schedule_segment<C, PAY, true>(P, cur, nxt, sid, scratch, st, bcast[0]);
+      schedule_segment_cta<C, PAY>(P, cur, nxt, sid, xk, st, bcast);
   } else {
-    U *scratch = reinterpret_cast<U *>(smem_raw) + warp * (kMaxSample + 1);
-    const uint32_t nwarps = gridDim.x * (kThreads / 32);
-    for (uint32_t sid = blockIdx.x * (kThreads / 32) + warp; sid < nseg; sid += nwarps)
-      schedule_segment<C, PAY, false>(P, cur, nxt, sid, scratch, st, bcast[warp]);
+    const uint32_t per_round = gridDim.x * (kThreads / 32);
+    for (uint32_t base = blockIdx.x * (kThreads / 32); base < nseg; base += per_round) {
+      const uint32_t sid = base + (threadIdx.x >> 5);
+      schedule_round_warp<C, PAY>(P, cur, nxt, sid, sid < nseg, st, rs);
+    }
   }
   __syncthreads();
   if (threadIdx.x < ST_COUNT && st[threadIdx.x]) {
