@@ -30,7 +30,7 @@ class TsqParams(ctypes.Structure):
     _fields_ = [("dran", ctypes.c_double), ("mitigation", ctypes.c_int32),
                 ("fast_paths", ctypes.c_int32), ("max_depth", ctypes.c_int32),
                 ("host_levels", ctypes.c_int32), ("small_threshold", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("reserved", ctypes.c_int64 * 3)]
+                ("reproducible", ctypes.c_int32), ("reserved", ctypes.c_int64 * 3)]
 
 
 class TsqStats(ctypes.Structure):

@@ -56,12 +56,20 @@ class GpuConfig:
     host_levels  drive recursion levels from the host with a per-level trace
                  (debug / measurement); the default runs the whole recursion
                  inside one CUDA graph with a device-side loop.
+    reproducible place every tile's < and > runs by decoupled look-back, so
+                 the layout of each level -- and with it the children's pivot
+                 samples, the stats and the order of equal-key records -- is
+                 identical run to run.  The default reserves each tile's
+                 ranges with one atomic instead: sorted keys are the same,
+                 the placement of equal-key payloads and the stage counts may
+                 differ between runs.
     """
 
     fast_paths: bool = True
     max_depth: int = 96
     host_levels: bool = False
     small_threshold: int = 4096
+    reproducible: bool = False
 
     def __post_init__(self):
         if not 1 <= self.small_threshold <= 4096:

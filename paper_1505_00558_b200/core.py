@@ -360,6 +360,7 @@ class Sorter:
         p.fast_paths = 1 if self.gpu.fast_paths else 0
         p.max_depth = self.gpu.max_depth
         p.small_threshold = self.gpu.small_threshold
+        p.reproducible = 1 if self.gpu.reproducible else 0
         p.host_levels = 1 if (self.gpu.host_levels or self.stage_hook is not None) else 0
         ts = N.TsqStats()
         dev = job.keys.device

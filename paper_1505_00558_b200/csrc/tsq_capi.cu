@@ -236,6 +236,7 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
   p->mitigation = 1;
   p->dran = 1.0;
   p->small_t = kSmallT;
+  p->reproducible = 0;
 }
 
 tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
@@ -525,6 +526,7 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   pv.dran = pp.dran > 0.0 ? pp.dran : 1.0;
   pv.mitigation = pp.mitigation;
   pv.fast_paths = pp.fast_paths;
+  pv.reproducible = pp.reproducible != 0;
   pv.max_depth = pp.max_depth > 0 ? pp.max_depth : 96;
   TSQ_CUDA(cudaStreamWaitEvent(s, ws->done, 0));
 

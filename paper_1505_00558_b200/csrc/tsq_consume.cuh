@@ -43,9 +43,12 @@ __device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T
   }
 }
 
-// per-stage counts of each consumer warp's keys: <, ==, >
+// per-stage counts of each consumer warp's keys (<, ==, >) and, per
+// consumer thread, the (<, >, valid) counts of the lanes before it in its
+// warp, packed 10 bits each
 struct StageCounts {
   uint32_t w[kConsumerWarps][3];
+  uint32_t t[kConsumers];
 };
 
 // class of key x against the pivot: 0 <, 1 ==, 2 >, 3 outside the segment
@@ -54,14 +57,46 @@ __device__ __forceinline__ uint32_t key_class(U x, U piv, bool valid) {
   return ((uint32_t)(x >= piv) + (uint32_t)(x > piv)) | (valid ? 0u : 3u);
 }
 
+// one consumer warp's keys of a stage, counted by a counter lane in the
+// order the consumer will rank them; FULL: the whole tile is the segment's
+template <class C, bool PAY, bool FULL>
+__device__ __forceinline__ void count_slice(const typename C::U *sk, int w, int lane, bool raw,
+                                            typename C::U piv, int rlo, int rhi, uint32_t &lt,
+                                            uint32_t &gt, uint32_t &va) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
+    U key[G::VN];
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) {
+      const U x = raw ? C::enc(key[q]) : key[q];
+      if (FULL) {
+        lt += x < piv ? 1u : 0u;
+        gt += x > piv ? 1u : 0u;
+      } else {
+        const int idx = e0 + q;
+        const bool valid = idx >= rlo && idx < rhi;
+        lt += (valid && x < piv) ? 1u : 0u;
+        gt += (valid && x > piv) ? 1u : 0u;
+        va += valid ? 1u : 0u;
+      }
+    }
+  }
+  if (FULL) va = G::IPT;
+}
+
 template <class C, bool PAY>
 __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typename C::U *in_k,
-                                             u64 *full, u64 *aggr, u64 *empty, StageMeta *meta,
-                                             StageCounts *sc, int cw,
+                                             u64 *full, u64 *aggr, u64 *ready, u64 *empty,
+                                             StageMeta *meta, StageCounts *sc, int cw,
                                              const volatile uint32_t *done_iter) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   const int lane = threadIdx.x & 31;
+  const bool reproducible = P->reproducible != 0;
   const uint32_t level = P->ctl->level;
   (void)level;
   for (uint32_t it = (uint32_t)cw;; it += kCounterWarps) {
@@ -97,32 +132,28 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       // each consumer warp's keys, in the order it will rank them
       const U piv = (U)m.pivot;
       const bool full_tile = rlo == 0 && rhi == G::TILE;
-      uint32_t tl = 0, tg = 0;
+      uint32_t tl = 0, tg = 0, tv = 0;
 #pragma unroll 1
       for (int w = 0; w < kConsumerWarps; ++w) {
         uint32_t lt = 0, gt = 0, va = 0;
+        if (full_tile)
+          count_slice<C, PAY, true>(sk, w, lane, raw, piv, rlo, rhi, lt, gt, va);
+        else
+          count_slice<C, PAY, false>(sk, w, lane, raw, piv, rlo, rhi, lt, gt, va);
+        // at most 32 * IPT = 512 per class: three 10-bit counts, scanned
+        // across the lanes; each consumer thread gets its exclusive prefix
+        const uint32_t own = lt | (gt << 10) | (va << 20);
+        uint32_t pk = own;
 #pragma unroll
-        for (int v = 0; v < G::VPT; ++v) {
-          const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
-          U key[G::VN];
-          unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
-#pragma unroll
-          for (int q = 0; q < G::VN; ++q) {
-            const int idx = e0 + q;
-            const U x = raw ? C::enc(key[q]) : key[q];
-            const bool valid = full_tile || (idx >= rlo && idx < rhi);
-            lt += (valid && x < piv) ? 1u : 0u;
-            gt += (valid && x > piv) ? 1u : 0u;
-            va += valid ? 1u : 0u;
-          }
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, pk, o);
+          if (lane >= o) pk += y;
         }
-        // at most 32 * IPT = 512 per class: pack three 11-bit counts
-        uint32_t pk = lt | (gt << 11) | (va << 22);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) pk += __shfl_xor_sync(0xffffffffu, pk, o);
-        lt = pk & 0x7ffu;
-        gt = (pk >> 11) & 0x7ffu;
-        va = pk >> 22;
+        sc[s].t[w * 32 + lane] = pk - own;
+        pk = __shfl_sync(0xffffffffu, pk, 31);
+        lt = pk & 0x3ffu;
+        gt = (pk >> 10) & 0x3ffu;
+        va = pk >> 20;
         if (lane == 0) {
           sc[s].w[w][0] = lt;
           sc[s].w[w][1] = va - lt - gt;
@@ -130,18 +161,69 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
         }
         tl += lt;
         tg += gt;
+        tv += va;
       }
       if (lane == 0) {
         const u64 agg = ((u64)tl << 31) | (u64)tg;
         m.agg = agg;
-        st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
+        if (reproducible) {
+          st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
+        } else {
+          // reserve the tile's < and > ranges of its segment in one atomic
+          // on the segment's fill word (first tile's descriptor slot)
+          m.excl = atomicAdd(reinterpret_cast<unsigned long long *>(
+                                 &P->lookback[cur][m.tile_base]), agg);
+          if (PAY) m.eq_excl = atomicAdd(&P->segs[cur][m.sid].eq_fill, tv - tl - tg);
+          TSQ_MARK(level, t, 4);
+        }
         TSQ_MARK(level, t, 3);
       }
     }
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive(&aggr[s]);
+      // reproducible: the look-back warp resolves the offsets; otherwise
+      // the reservation above did and the consumers may go
+      mbar_arrive(reproducible ? &aggr[s] : &ready[s]);
       mbar_arrive(&empty[s]);  // done reading the stage
+    }
+  }
+}
+
+// Stage one consumer thread's keys of a tile into the out buffer: each key
+// goes to the thread's next < slot (counting up) or next > slot (counting
+// down); records also stage the == payloads.  MODE 0: both buffers hold
+// encoded keys, 1: source raw, 2: destination raw, 3: both raw.
+template <class C, bool PAY, bool FULL, int MODE>
+__device__ __forceinline__ void stage_keys(const typename C::U *sk, const uint32_t *sp, int tid,
+                                           typename C::U piv, int rlo, int rhi, uint32_t plt,
+                                           uint32_t pgt, uint32_t peq, typename C::U *ok,
+                                           uint32_t *op) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + tid) * G::VN;
+    U key[G::VN];
+    uint32_t pay[G::VN];
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay);
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) {
+      const U x = (MODE & 1) ? C::enc(key[q]) : key[q];
+      const U y = MODE == 2 ? C::dec(key[q]) : (MODE == 1 ? x : key[q]);
+      const bool valid = FULL || (e0 + q >= rlo && e0 + q < rhi);
+      const bool is_lt = valid && x < piv, is_gt = valid && x > piv;
+      if (PAY) {
+        const uint32_t pos = is_lt ? plt : (is_gt ? pgt : peq);
+        if (is_lt || is_gt) ok[pos] = y;
+        if (valid) op[pos] = pay[q];
+        peq += (valid && !is_lt && !is_gt) ? 1u : 0u;
+      } else {
+        const uint32_t pos = is_lt ? plt : pgt;
+        if (is_lt || is_gt) ok[pos] = y;
+      }
+      plt += is_lt ? 1u : 0u;
+      pgt -= is_gt ? 1u : 0u;
     }
   }
 }
@@ -183,7 +265,8 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const ty
   const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
   const long long D_lt = begin + ex_lt;                    // first slot of this tile's < run
   const long long D_gt = m.end - ex_gt - (long long)t_gt;  // first slot of its > run
-  const long long D_eq = lo - ex_lt - ex_gt;               // records: side-buffer slot
+  // records: the tile's first == payload slot in the side buffer
+  const long long D_eq = P->reproducible ? lo - ex_lt - ex_gt : begin + (long long)m.eq_excl;
   const int o_lt = (int)(D_lt & (kAlign - 1));
   const int g_base = (o_lt + (int)t_lt + kAlign - 1) & ~(kAlign - 1);
   const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
@@ -193,39 +276,25 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const ty
   const uint32_t *sp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
   const U piv = (U)m.pivot;
   const int rlo = (int)(lo - m.tstart), rhi = (int)(m.hi - m.tstart);
-  const bool full_tile = rlo == 0 && rhi == G::TILE;
-  const uint32_t lmask = (1u << lane) - 1u;
-  uint32_t lt0 = (uint32_t)o_lt + w_lt;              // next < slot of this warp
-  uint32_t gt0 = (uint32_t)o_gt + t_gt - 1u - w_gt;  // next > slot (filled backwards)
-  uint32_t eq0 = (uint32_t)o_eq + w_eq;
-#pragma unroll
-  for (int v = 0; v < G::VPT; ++v) {
-    const int e0 = (v * kConsumers + tid) * G::VN;
-    U key[G::VN];
-    uint32_t pay[G::VN];
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
-    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay);
-#pragma unroll
-    for (int q = 0; q < G::VN; ++q) {
-      const int idx = e0 + q;
-      const U x = src_raw ? C::enc(key[q]) : key[q];
-      const uint32_t cl = key_class<U>(x, piv, full_tile || (idx >= rlo && idx < rhi));
-      const uint32_t blt = __ballot_sync(0xffffffffu, cl == 0);
-      const uint32_t bgt = __ballot_sync(0xffffffffu, cl == 2);
-      const uint32_t beq = PAY ? __ballot_sync(0xffffffffu, cl == 1) : 0u;
-      // branch-free slot selection, predicated stores
-      const uint32_t p_lt = lt0 + __popc(blt & lmask);
-      const uint32_t p_gt = gt0 - __popc(bgt & lmask);
-      uint32_t pos = cl == 0u ? p_lt : p_gt;
-      if (PAY) pos = cl == 1u ? eq0 + __popc(beq & lmask) : pos;
-      U y = key[q];
-      if (src_raw != dst_raw) y = src_raw ? C::enc(y) : C::dec(y);
-      if ((cl & 1u) == 0u) ok[pos] = y;  // cl == 0 or cl == 2
-      if (PAY && cl != 3u) op[pos] = pay[q];
-      lt0 += __popc(blt);
-      gt0 -= __popc(bgt);
-      if (PAY) eq0 += __popc(beq);
-    }
+  // this thread's first slots: warp offset + the counter's per-lane prefix
+  const uint32_t pre = c.t[tid];
+  const uint32_t e_lt = pre & 0x3ffu, e_gt = (pre >> 10) & 0x3ffu, e_va = pre >> 20;
+  uint32_t plt = (uint32_t)o_lt + w_lt + e_lt;              // next < slot
+  uint32_t pgt = (uint32_t)o_gt + t_gt - 1u - w_gt - e_gt;  // next > slot (backwards)
+  uint32_t peq = (uint32_t)o_eq + w_eq + (e_va - e_lt - e_gt);
+  const bool full = rlo == 0 && rhi == G::TILE;
+  if (src_raw && dst_raw) {
+    if (full) stage_keys<C, PAY, true, 3>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    else stage_keys<C, PAY, false, 3>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+  } else if (src_raw) {
+    if (full) stage_keys<C, PAY, true, 1>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    else stage_keys<C, PAY, false, 1>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+  } else if (dst_raw) {
+    if (full) stage_keys<C, PAY, true, 2>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    else stage_keys<C, PAY, false, 2>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+  } else {
+    if (full) stage_keys<C, PAY, true, 0>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    else stage_keys<C, PAY, false, 0>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
   }
   // the stage is no longer needed: hand it back to the producer
   __syncwarp();
@@ -285,7 +354,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
     return;
   }
   if (warp >= kCounterWarp) {
-    counter_loop<C, PAY>(P, cur, in_k, full, aggr, empty, meta, sc, warp - kCounterWarp,
+    counter_loop<C, PAY>(P, cur, in_k, full, aggr, ready, empty, meta, sc, warp - kCounterWarp,
                          &done_iter);
     return;
   }

@@ -39,7 +39,8 @@ struct Seg {
   u64 pivot;
   uint32_t tile_base, ntiles;
   uint32_t buf, kind, depth, noverify;
-  uint32_t done, fail;
+  uint32_t eq_fill;  // records, atomic placement: == payload slots reserved so far
+  uint32_t fail;
 };
 
 // A segment of <= kSmallT elements waiting for the on-chip sort.
@@ -89,6 +90,7 @@ struct Params {
   int aligned[2];         // buffer's key / payload pointers are 16B aligned
   int single_stage;       // tsq_partition_segment: one given-pivot stage
   int small_t;            // segments <= small_t go to the on-chip sort
+  int reproducible;       // look-back placement (else atomic range reservation)
   u64 given_pivot;        // encoded pivot for single_stage
   Seg *segs[2];
   uint32_t *tilemap[2];
@@ -282,6 +284,10 @@ __device__ __forceinline__ void bulk_commit() {
 }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// all but the most recent bulk-store group have finished reading smem
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

@@ -78,6 +78,7 @@ struct StageMeta {
   long long tstart, lo, hi, begin, end;
   u64 pivot, next_key, agg, excl;
   uint32_t t, k, kind, buf, tile_base, sid, skip, has_next;
+  uint32_t eq_excl;  // records, atomic placement: this tile's first == side slot
 };
 
 }  // namespace tsq
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
       Seg s;
       s.begin = 0; s.end = n; s.pivot = piv;
       s.tile_base = 0; s.ntiles = ntiles;
-      s.buf = buf; s.kind = kind; s.depth = 1; s.noverify = 0; s.done = 0; s.fail = 0;
+      s.buf = buf; s.kind = kind; s.depth = 1; s.noverify = 0; s.eq_fill = 0; s.fail = 0;
       pv.segs[0][0] = s;
       ctl->cur_nseg = 1;
       ctl->cur_ntiles = ntiles;

@@ -182,6 +182,7 @@ __device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long lon
 __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
                                               StageMeta *meta, int lw,
                                               const volatile uint32_t *done_iter) {
+  if (!P->reproducible) return;  // the counter warps reserve ranges instead
   const int lane = threadIdx.x & 31;
   u64 *lb = P->lookback[cur];
   const uint32_t level = P->ctl->level;

@@ -269,7 +269,9 @@ __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u
     }
     return false;
   }
-  const u64 inc = P->lookback[cur][sg.tile_base + sg.ntiles - 1];
+  // the segment's (<, >) totals: the last tile's inclusive descriptor, or
+  // the fill word all its tiles reserved from
+  const u64 inc = P->lookback[cur][sg.tile_base + (P->reproducible ? sg.ntiles - 1 : 0)];
   const long long lt = (long long)((inc >> 31) & 0x7fffffffull);
   const long long gt = (long long)(inc & 0x7fffffffull);
   const long long eq = len - lt - gt;
@@ -469,7 +471,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
           s.begin = q.begin; s.end = q.end; s.pivot = q.pivot;
           s.tile_base = ltile; s.ntiles = q.ntiles;
           s.buf = q.buf; s.kind = q.kind; s.depth = q.depth; s.noverify = q.noverify;
-          s.done = 0; s.fail = 0;
+          s.eq_fill = 0; s.fail = 0;
           P->segs[nxt][lslot] = s;
         }
         uint32_t *tm = P->tilemap[nxt] + ltile;
@@ -518,7 +520,7 @@ __device__ void cta_append_level(const Params *P, int nxt, long long begin, long
       s.begin = begin; s.end = end; s.pivot = pivot;
       s.tile_base = tbase; s.ntiles = ntiles;
       s.buf = buf; s.kind = kind; s.depth = depth; s.noverify = noverify;
-      s.done = 0; s.fail = 0;
+      s.eq_fill = 0; s.fail = 0;
       P->segs[nxt][slot] = s;
     } else {
       atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);

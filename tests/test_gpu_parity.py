@@ -47,9 +47,10 @@ def _random(dtype, n, rng, vmax=None):
     return rng.integers(lo, hi, n, dtype=dt, endpoint=True)
 
 
-@pytest.fixture(scope="module")
-def sorter(cuda_ok):
-    return T.Sorter(seed=1)
+@pytest.fixture(scope="module", params=[False, True], ids=["reserve", "reproducible"])
+def sorter(cuda_ok, request):
+    # both placements: atomic range reservation (default) and look-back
+    return T.Sorter(seed=1, gpu=T.GpuConfig(reproducible=request.param))
 
 
 @pytest.mark.parametrize("n", [2, 3, 17, 100, 4095, 4096, 4097, 8193, 65536, 100003, 1 << 20])
@@ -239,9 +240,9 @@ def test_negative_zero_and_nan_total_order(sorter):
 def test_host_levels_trace_matches_graph(cuda_ok):
     x = np.random.default_rng(4).integers(-2**31, 2**31, 1 << 21, dtype=np.int64).astype(np.int32)
     a, b = _dev(x), _dev(x)
-    s1 = T.Sorter(seed=3)
+    s1 = T.Sorter(seed=3, gpu=T.GpuConfig(reproducible=True))
     st1 = s1.sort_with_stats(a)
-    s2 = T.Sorter(seed=3, gpu=T.GpuConfig(host_levels=True))
+    s2 = T.Sorter(seed=3, gpu=T.GpuConfig(host_levels=True, reproducible=True))
     st2 = s2.sort_with_stats(b)
     assert torch.equal(a, b)
     assert st1.stages == st2.stages and st1.max_depth == st2.max_depth
@@ -252,8 +253,9 @@ def test_host_levels_trace_matches_graph(cuda_ok):
 def test_determinism_and_stats(cuda_ok):
     x = np.random.default_rng(6).integers(0, 10**6, 500000).astype(np.int32)
     a, b = _dev(x), _dev(x)
-    st1 = T.Sorter(seed=77).sort_with_stats(a)
-    st2 = T.Sorter(seed=77).sort_with_stats(b)
+    g = T.GpuConfig(reproducible=True)
+    st1 = T.Sorter(seed=77, gpu=g).sort_with_stats(a)
+    st2 = T.Sorter(seed=77, gpu=g).sort_with_stats(b)
     assert torch.equal(a, b)
     assert st1.as_dict() == st2.as_dict()
     assert st1.element_writes == st1.array_writes + st1.scratch_writes
