@@ -60,11 +60,11 @@ __device__ __forceinline__ uint32_t key_class(U x, U piv, bool valid) {
 // one consumer warp's keys of a stage, counted by a counter lane in the
 // order the consumer will rank them; FULL: the whole tile is the segment's
 template <class C, bool PAY, bool FULL>
-__device__ __forceinline__ void count_slice(const typename C::U *sk, int w, int lane, bool raw,
-                                            typename C::U piv, int rlo, int rhi, uint32_t &lt,
-                                            uint32_t &gt, uint32_t &va) {
+__device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, int lane, bool raw,
+                                                typename C::U piv, int rlo, int rhi) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
+  uint32_t lt = 0, gt = 0, va = 0;
 #pragma unroll
   for (int v = 0; v < G::VPT; ++v) {
     const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
@@ -86,6 +86,7 @@ __device__ __forceinline__ void count_slice(const typename C::U *sk, int w, int 
     }
   }
   if (FULL) va = G::IPT;
+  return lt | (gt << 10) | (va << 20);
 }
 
 template <class C, bool PAY>
@@ -129,31 +130,42 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       }
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&P->segs[cur][m.sid].fail, 1u);
     } else {
-      // each consumer warp's keys, in the order it will rank them
+      // each consumer warp's keys, in the order it will rank them: all eight
+      // slices counted first, then their lane scans interleaved (ILP)
       const U piv = (U)m.pivot;
-      const bool full_tile = rlo == 0 && rhi == G::TILE;
-      uint32_t tl = 0, tg = 0, tv = 0;
-#pragma unroll 1
-      for (int w = 0; w < kConsumerWarps; ++w) {
-        uint32_t lt = 0, gt = 0, va = 0;
-        if (full_tile)
-          count_slice<C, PAY, true>(sk, w, lane, raw, piv, rlo, rhi, lt, gt, va);
-        else
-          count_slice<C, PAY, false>(sk, w, lane, raw, piv, rlo, rhi, lt, gt, va);
-        // at most 32 * IPT = 512 per class: three 10-bit counts, scanned
-        // across the lanes; each consumer thread gets its exclusive prefix
-        const uint32_t own = lt | (gt << 10) | (va << 20);
-        uint32_t pk = own;
+      uint32_t own[kConsumerWarps], inc[kConsumerWarps];
+      if (rlo == 0 && rhi == G::TILE) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, pk, o);
-          if (lane >= o) pk += y;
+        for (int w = 0; w < kConsumerWarps; ++w)
+          own[w] = count_slice<C, PAY, true>(sk, w, lane, raw, piv, rlo, rhi);
+      } else {
+        // partial tiles (segment ends): compact code, not unrolled
+#pragma unroll 1
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          const uint32_t x = count_slice<C, PAY, false>(sk, w, lane, raw, piv, rlo, rhi);
+#pragma unroll
+          for (int u = 0; u < kConsumerWarps; ++u)
+            if (u == w) own[u] = x;
         }
-        sc[s].t[w * 32 + lane] = pk - own;
-        pk = __shfl_sync(0xffffffffu, pk, 31);
-        lt = pk & 0x3ffu;
-        gt = (pk >> 10) & 0x3ffu;
-        va = pk >> 20;
+      }
+      // at most 32 * IPT = 512 per class: three 10-bit counts, scanned
+      // across the lanes; each consumer thread gets its exclusive prefix
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) inc[w] = own[w];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc[w], o);
+          if (lane >= o) inc[w] += y;
+        }
+      }
+      uint32_t tl = 0, tg = 0, tv = 0;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        sc[s].t[w * 32 + lane] = inc[w] - own[w];
+        const uint32_t pk = __shfl_sync(0xffffffffu, inc[w], 31);
+        const uint32_t lt = pk & 0x3ffu, gt = (pk >> 10) & 0x3ffu, va = pk >> 20;
         if (lane == 0) {
           sc[s].w[w][0] = lt;
           sc[s].w[w][1] = va - lt - gt;
@@ -171,9 +183,11 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
         } else {
           // reserve the tile's < and > ranges of its segment in one atomic
           // on the segment's fill word (first tile's descriptor slot)
-          m.excl = atomicAdd(reinterpret_cast<unsigned long long *>(
-                                 &P->lookback[cur][m.tile_base]), agg);
-          if (PAY) m.eq_excl = atomicAdd(&P->segs[cur][m.sid].eq_fill, tv - tl - tg);
+          const u64 ex = atomicAdd(reinterpret_cast<unsigned long long *>(
+                                       &P->lookback[cur][m.tile_base]), agg);
+          const uint32_t eqx = PAY ? atomicAdd(&P->segs[cur][m.sid].eq_fill, tv - tl - tg) : 0u;
+          m.excl = ex;
+          m.eq_excl = eqx;
           TSQ_MARK(level, t, 4);
         }
         TSQ_MARK(level, t, 3);

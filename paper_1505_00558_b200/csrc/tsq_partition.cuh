@@ -27,10 +27,36 @@
 // complete in, so the consumers rarely wait for offsets.
 #pragma once
 
+#ifndef TSQ_CLAIM_AHEAD
+#define TSQ_CLAIM_AHEAD 0
+#endif
+
 namespace tsq {
 
 // ---------------------------------------------------------------------------
 // Producer warp.
+
+// A claimed tile and the fields of its segment the producer needs.
+struct Claim {
+  uint32_t t, sid, tile_base, kind, buf;
+  long long begin, end;
+  u64 pivot;
+};
+
+__device__ __forceinline__ Claim claim_tile(const Params *P, int cur, Ctl *ctl, uint32_t ntiles) {
+  const int lane = threadIdx.x & 31;
+  Claim c;
+  uint32_t t = 0;
+  if (lane == 0) t = atomicAdd(&ctl->tile_ticket, 1u);
+  c.t = __shfl_sync(0xffffffffu, t, 0);
+  if (c.t >= ntiles) return c;
+  c.sid = P->tilemap[cur][c.t];
+  const Seg *sgp = &P->segs[cur][c.sid];
+  c.begin = sgp->begin; c.end = sgp->end;
+  c.tile_base = sgp->tile_base; c.kind = sgp->kind; c.buf = sgp->buf;
+  c.pivot = sgp->pivot;
+  return c;
+}
 
 template <class C, bool PAY>
 __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t ntiles,
@@ -43,35 +69,44 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
   Ctl *ctl = P->ctl;
   const uint32_t level = ctl->level;
   (void)level;
+  // Reservation mode: claim (and resolve) the next tile while the ring is
+  // full, so the claim's round trips hide behind the wait for a free stage.
+  // Look-back mode claims only once a stage is free, so claim order tracks
+  // processing order across CTAs (a look-back waits on its predecessors).
+  const bool ahead = TSQ_CLAIM_AHEAD && !P->reproducible;
+  Claim c;
+  if (ahead) {
+    c = claim_tile(P, cur, ctl, ntiles);
+    if (c.t >= ntiles) {
+      if (lane == 0) *done_iter = 0;
+      return;
+    }
+  }
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
     const uint32_t j = it / kStages;
-    // claim a tile only once a stage is free for it, so claim order tracks
-    // processing order across CTAs (the look-back waits on predecessors)
     if (j > 0) wait_empty_producer(&empty[s], (j - 1) & 1u);
-    uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(&ctl->tile_ticket, 1u);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    StageMeta &m = meta[s];
-    if (t >= ntiles) {
-      // iteration `it` and later have no tile: every role stops there
-      if (lane == 0) *done_iter = it;
-      return;
+    if (!ahead) {
+      c = claim_tile(P, cur, ctl, ntiles);
+      if (c.t >= ntiles) {
+        // iteration `it` and later have no tile: every role stops there
+        if (lane == 0) *done_iter = it;
+        return;
+      }
     }
+    const uint32_t t = c.t;
+    StageMeta &m = meta[s];
     TSQ_MARK(level, t, 0);
-    const uint32_t sid = P->tilemap[cur][t];
-    const Seg *sgp = &P->segs[cur][sid];
-    const long long begin = sgp->begin, end = sgp->end;
-    const uint32_t tile_base = sgp->tile_base, kind = sgp->kind, buf = sgp->buf;
-    const u64 pivot = sgp->pivot;
-    const uint32_t k = t - tile_base;
+    const long long begin = c.begin, end = c.end;
+    const uint32_t kind = c.kind, buf = c.buf;
+    const uint32_t k = t - c.tile_base;
     const long long tstart = (begin / G::TILE + k) * (long long)G::TILE;
     const long long lo = tstart > begin ? tstart : begin;
     const long long hi = (tstart + G::TILE) < end ? (tstart + G::TILE) : end;
     const U *src = reinterpret_cast<const U *>(P->keys[buf]);
     const uint32_t *psrc = PAY ? P->pay[buf] : nullptr;
     uint32_t skip = 0;
-    if (kind != KIND_PARTITION) skip = ld_volatile32(&sgp->fail) != 0 ? 1u : 0u;
+    if (kind != KIND_PARTITION) skip = ld_volatile32(&P->segs[cur][c.sid].fail) != 0 ? 1u : 0u;
     U *dk = in_k + (size_t)s * G::TILE;
     uint32_t *dp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
     uint32_t tx = 0;
@@ -98,8 +133,8 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
     __syncwarp();
     if (lane == 0) {
       m.tstart = tstart; m.lo = lo; m.hi = hi; m.begin = begin; m.end = end;
-      m.pivot = pivot;
-      m.t = t; m.k = k; m.kind = kind; m.buf = buf; m.tile_base = tile_base; m.sid = sid;
+      m.pivot = c.pivot;
+      m.t = t; m.k = k; m.kind = kind; m.buf = buf; m.tile_base = c.tile_base; m.sid = c.sid;
       m.skip = skip;
       m.has_next = 0;
       if (kind != KIND_PARTITION && !skip && hi < end) {
@@ -115,6 +150,13 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
         if (PAY) bulk_load(dp + (a0 - tstart), psrc + a0, (uint32_t)((a1 - a0) * 4), &full[s]);
       } else {
         mbar_arrive(&full[s]);
+      }
+    }
+    if (ahead) {
+      c = claim_tile(P, cur, ctl, ntiles);
+      if (c.t >= ntiles) {
+        if (lane == 0) *done_iter = it + 1;
+        return;
       }
     }
   }
