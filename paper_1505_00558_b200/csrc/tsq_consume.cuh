@@ -89,33 +89,58 @@ __device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, 
   return lt | (gt << 10) | (va << 20);
 }
 
+// Per-stage scratch of the counter warps: each one's share of the tile's
+// (<, >, valid) totals and the count of warps done with the stage.
+struct CounterShare {
+  uint32_t lt[kCounterWarps], gt[kCounterWarps], va[kCounterWarps];
+  uint32_t finished;
+};
+
+// Counter warps: all kCounterWarps warps take every tile, warp cw counting
+// the slices of consumer warps [cw * kSlices, (cw + 1) * kSlices) -- a tile
+// is counted in a quarter of the time one warp would take.  The warp that
+// finishes a tile last combines the shares and either reserves the tile's
+// output ranges with one atomic (default) or publishes its aggregate for
+// the look-back warps (reproducible mode).
 template <class C, bool PAY>
 __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typename C::U *in_k,
                                              u64 *full, u64 *aggr, u64 *ready, u64 *empty,
-                                             StageMeta *meta, StageCounts *sc, int cw,
-                                             const volatile uint32_t *done_iter) {
+                                             StageMeta *meta, StageCounts *sc, CounterShare *cs,
+                                             int cw) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
+  constexpr int kSlices = kConsumerWarps / kCounterWarps;
   const int lane = threadIdx.x & 31;
   const bool reproducible = P->reproducible != 0;
   const uint32_t level = P->ctl->level;
   (void)level;
-  for (uint32_t it = (uint32_t)cw;; it += kCounterWarps) {
+  for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
-    if (!wait_or_done(&full[s], (it / kStages) & 1u, done_iter, it)) return;
+    wait_full_consumer(&full[s], (it / kStages) & 1u);
     StageMeta &m = meta[s];
+    if (m.kind == KIND_DONE) {
+      // out of tiles: the last counter warp here passes the marker on
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&cs[s].finished, 1u) == kCounterWarps - 1)
+          mbar_arrive(reproducible ? &aggr[s] : &ready[s]);
+      }
+      return;
+    }
     const uint32_t t = m.t;
-    if (lane == 0) TSQ_MARK(level, t, 2);
+    if (lane == 0 && cw == 0) TSQ_MARK(level, t, 2);
     const U *sk = in_k + (size_t)s * G::TILE;
     const bool raw = P->raw[m.buf] != 0;
     const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
-    if (m.kind != KIND_PARTITION) {
+    const bool part = m.kind == KIND_PARTITION;
+    if (!part) {
       // verification: every pair (i, i+1) of the segment's keys in this tile,
       // the last one against the first key of the next tile
       bool bad = false;
       if (!m.skip) {
         const bool asc = m.kind == KIND_VERIFY_ASC;
-        for (int i = rlo + lane; i < rhi; i += 32) {
+        for (int i = rlo + cw * 32 + lane; i < rhi; i += 32 * kCounterWarps) {
           U a = sk[i], b;
           bool have = true;
           if (i + 1 < rhi) b = sk[i + 1];
@@ -130,41 +155,37 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       }
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&P->segs[cur][m.sid].fail, 1u);
     } else {
-      // each consumer warp's keys, in the order it will rank them: all eight
-      // slices counted first, then their lane scans interleaved (ILP)
+      // this warp's consumer slices, in the order the consumers rank them;
+      // all counted first, then their lane scans interleaved
       const U piv = (U)m.pivot;
-      uint32_t own[kConsumerWarps], inc[kConsumerWarps];
+      uint32_t own[kSlices], inc[kSlices];
       if (rlo == 0 && rhi == G::TILE) {
 #pragma unroll
-        for (int w = 0; w < kConsumerWarps; ++w)
-          own[w] = count_slice<C, PAY, true>(sk, w, lane, raw, piv, rlo, rhi);
+        for (int j = 0; j < kSlices; ++j)
+          own[j] = count_slice<C, PAY, true>(sk, cw * kSlices + j, lane, raw, piv, rlo, rhi);
       } else {
-        // partial tiles (segment ends): compact code, not unrolled
-#pragma unroll 1
-        for (int w = 0; w < kConsumerWarps; ++w) {
-          const uint32_t x = count_slice<C, PAY, false>(sk, w, lane, raw, piv, rlo, rhi);
 #pragma unroll
-          for (int u = 0; u < kConsumerWarps; ++u)
-            if (u == w) own[u] = x;
-        }
+        for (int j = 0; j < kSlices; ++j)
+          own[j] = count_slice<C, PAY, false>(sk, cw * kSlices + j, lane, raw, piv, rlo, rhi);
       }
       // at most 32 * IPT = 512 per class: three 10-bit counts, scanned
       // across the lanes; each consumer thread gets its exclusive prefix
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) inc[w] = own[w];
+      for (int j = 0; j < kSlices; ++j) inc[j] = own[j];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
-        for (int w = 0; w < kConsumerWarps; ++w) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc[w], o);
-          if (lane >= o) inc[w] += y;
+        for (int j = 0; j < kSlices; ++j) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc[j], o);
+          if (lane >= o) inc[j] += y;
         }
       }
       uint32_t tl = 0, tg = 0, tv = 0;
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) {
-        sc[s].t[w * 32 + lane] = inc[w] - own[w];
-        const uint32_t pk = __shfl_sync(0xffffffffu, inc[w], 31);
+      for (int j = 0; j < kSlices; ++j) {
+        const int w = cw * kSlices + j;
+        sc[s].t[w * 32 + lane] = inc[j] - own[j];
+        const uint32_t pk = __shfl_sync(0xffffffffu, inc[j], 31);
         const uint32_t lt = pk & 0x3ffu, gt = (pk >> 10) & 0x3ffu, va = pk >> 20;
         if (lane == 0) {
           sc[s].w[w][0] = lt;
@@ -176,28 +197,48 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
         tv += va;
       }
       if (lane == 0) {
-        const u64 agg = ((u64)tl << 31) | (u64)tg;
-        m.agg = agg;
-        if (reproducible) {
-          st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
-        } else {
-          // reserve the tile's < and > ranges of its segment in one atomic
-          // on the segment's fill word (first tile's descriptor slot)
-          const u64 ex = atomicAdd(reinterpret_cast<unsigned long long *>(
-                                       &P->lookback[cur][m.tile_base]), agg);
-          const uint32_t eqx = PAY ? atomicAdd(&P->segs[cur][m.sid].eq_fill, tv - tl - tg) : 0u;
-          m.excl = ex;
-          m.eq_excl = eqx;
-          TSQ_MARK(level, t, 4);
-        }
-        TSQ_MARK(level, t, 3);
+        cs[s].lt[cw] = tl;
+        cs[s].gt[cw] = tg;
+        cs[s].va[cw] = tv;
       }
     }
     __syncwarp();
     if (lane == 0) {
-      // reproducible: the look-back warp resolves the offsets; otherwise
-      // the reservation above did and the consumers may go
-      mbar_arrive(reproducible ? &aggr[s] : &ready[s]);
+      // the last counter warp done with the stage hands it on
+      __threadfence_block();
+      const bool last = atomicAdd(&cs[s].finished, 1u) == kCounterWarps - 1;
+      if (last) {
+        __threadfence_block();
+        cs[s].finished = 0;
+        if (part) {
+          uint32_t tl = 0, tg = 0, tv = 0;
+#pragma unroll
+          for (int c = 0; c < kCounterWarps; ++c) {
+            tl += ld_volatile32(&cs[s].lt[c]);
+            tg += ld_volatile32(&cs[s].gt[c]);
+            tv += ld_volatile32(&cs[s].va[c]);
+          }
+          const u64 agg = ((u64)tl << 31) | (u64)tg;
+          m.agg = agg;
+          if (reproducible) {
+            st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
+          } else {
+            // reserve the tile's < and > ranges of its segment in one atomic
+            // on the segment's fill word (first tile's descriptor slot)
+            const u64 ex = atomicAdd(reinterpret_cast<unsigned long long *>(
+                                         &P->lookback[cur][m.tile_base]), agg);
+            const uint32_t eqx =
+                PAY ? atomicAdd(&P->segs[cur][m.sid].eq_fill, tv - tl - tg) : 0u;
+            m.excl = ex;
+            m.eq_excl = eqx;
+            TSQ_MARK(level, t, 4);
+          }
+          TSQ_MARK(level, t, 3);
+        }
+        // reproducible: the look-back warp resolves the offsets; otherwise
+        // the reservation above did and the consumers may go
+        mbar_arrive(reproducible ? &aggr[s] : &ready[s]);
+      }
       mbar_arrive(&empty[s]);  // done reading the stage
     }
   }
@@ -345,40 +386,41 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
   __shared__ __align__(8) u64 full[kStages], aggr[kStages], ready[kStages], empty[kStages];
   __shared__ StageMeta meta[kStages];
   __shared__ StageCounts sc[kStages];
-  __shared__ volatile uint32_t done_iter;
+  __shared__ CounterShare cshare[kStages];
 
   Ctl *ctl = P->ctl;
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u);
   const uint32_t ntiles = ctl->cur_ntiles;
   if (threadIdx.x == 0) {
-    done_iter = 0xffffffffu;
+    for (int s = 0; s < kStages; ++s) cshare[s].finished = 0;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&aggr[s], 1);
       mbar_init(&ready[s], 1);
-      mbar_init(&empty[s], kConsumerWarps + 1);  // consumers + the stage's counter warp
+      mbar_init(&empty[s], kConsumerWarps + kCounterWarps);  // consumers + counters
     }
     fence_barrier_init();
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   if (warp == kProducerWarp) {
-    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, empty, meta, &done_iter);
+    producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, aggr, empty, meta);
     return;
   }
   if (warp >= kCounterWarp) {
-    counter_loop<C, PAY>(P, cur, in_k, full, aggr, ready, empty, meta, sc, warp - kCounterWarp,
-                         &done_iter);
+    counter_loop<C, PAY>(P, cur, in_k, full, aggr, ready, empty, meta, sc, cshare,
+                         warp - kCounterWarp);
     return;
   }
   if (warp >= kLookbackWarp) {
-    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp, &done_iter);
+    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp);
     return;
   }
   for (uint32_t k = 0;; ++k) {
     const int s = (int)(k % kStages);
-    if (!wait_or_done(&ready[s], (k / kStages) & 1u, &done_iter, k)) break;
+    wait_ready_consumer(&ready[s], (k / kStages) & 1u);
+    if (meta[s].kind == KIND_DONE) break;
     unsigned char *ob = outb + (size_t)(k & 1u) * (G::OUT_K + G::OUT_P);
     emit_tile<C, PAY>(P, k, in_k, in_p, empty, meta, sc, reinterpret_cast<U *>(ob),
                       reinterpret_cast<uint32_t *>(ob + G::OUT_K));

@@ -27,7 +27,12 @@ constexpr u64 kFlagAgg = 1ull << 62;  // look-back: tile aggregate published
 constexpr u64 kFlagInc = 2ull << 62;  // look-back: inclusive prefix published
 constexpr u64 kValMask = (1ull << 62) - 1;
 
-enum SegKind : uint32_t { KIND_PARTITION = 0, KIND_VERIFY_ASC = 1, KIND_VERIFY_DESC = 2 };
+enum SegKind : uint32_t {
+  KIND_PARTITION = 0,
+  KIND_VERIFY_ASC = 1,
+  KIND_VERIFY_DESC = 2,
+  KIND_DONE = 3  // stage marker: the partition pass ran out of tiles
+};
 enum RunKind : uint32_t { RUN_EQ = 0, RUN_SORTED = 1, RUN_REVERSED = 2 };
 enum ErrFlag : uint32_t { ERR_DEPTH = 1u, ERR_CAPACITY = 2u, ERR_LEVELS = 4u };
 
@@ -240,28 +245,6 @@ __device__ __forceinline__ void wait_empty_producer(u64 *bar, uint32_t parity) {
   asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
 }
 #undef TSQ_WAIT_ASM
-
-// Wait for phase `parity` of `bar`, unless the level ends first: returns
-// false once *done_iter (the ring iteration at which the producer ran out of
-// tiles; ~0u while running) is <= it.
-__device__ __forceinline__ bool mbar_try_wait(u64 *bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 500;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ bool wait_or_done(u64 *bar, uint32_t parity,
-                                             const volatile uint32_t *done_iter, uint32_t it) {
-  for (;;) {
-    if (mbar_try_wait(bar, parity)) return true;
-    if (it >= *done_iter) return false;
-  }
-}
 
 // 1-D bulk copy global -> shared, completing `bytes` on the mbarrier
 // (cp.async.bulk: SASS UBLKCP); dst/src 16-byte aligned, bytes % 16 == 0

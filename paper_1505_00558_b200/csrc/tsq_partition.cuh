@@ -27,10 +27,6 @@
 // complete in, so the consumers rarely wait for offsets.
 #pragma once
 
-#ifndef TSQ_CLAIM_AHEAD
-#define TSQ_CLAIM_AHEAD 0
-#endif
-
 namespace tsq {
 
 // ---------------------------------------------------------------------------
@@ -61,38 +57,37 @@ __device__ __forceinline__ Claim claim_tile(const Params *P, int cur, Ctl *ctl, 
 template <class C, bool PAY>
 __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t ntiles,
                                               typename C::U *in_k, uint32_t *in_p, u64 *full,
-                                              u64 *empty, StageMeta *meta,
-                                              volatile uint32_t *done_iter) {
+                                              u64 *aggr, u64 *empty, StageMeta *meta) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   const int lane = threadIdx.x & 31;
   Ctl *ctl = P->ctl;
   const uint32_t level = ctl->level;
   (void)level;
-  // Reservation mode: claim (and resolve) the next tile while the ring is
-  // full, so the claim's round trips hide behind the wait for a free stage.
-  // Look-back mode claims only once a stage is free, so claim order tracks
-  // processing order across CTAs (a look-back waits on its predecessors).
-  const bool ahead = TSQ_CLAIM_AHEAD && !P->reproducible;
-  Claim c;
-  if (ahead) {
-    c = claim_tile(P, cur, ctl, ntiles);
-    if (c.t >= ntiles) {
-      if (lane == 0) *done_iter = 0;
-      return;
-    }
-  }
+  // a tile is claimed only once a stage is free for it, so claim order
+  // tracks processing order across CTAs (a look-back waits on predecessors)
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
     const uint32_t j = it / kStages;
     if (j > 0) wait_empty_producer(&empty[s], (j - 1) & 1u);
-    if (!ahead) {
-      c = claim_tile(P, cur, ctl, ntiles);
-      if (c.t >= ntiles) {
-        // iteration `it` and later have no tile: every role stops there
-        if (lane == 0) *done_iter = it;
-        return;
+    const Claim c = claim_tile(P, cur, ctl, ntiles);
+    if (c.t >= ntiles) {
+      // out of tiles: a DONE marker in the next stage stops every role.  The
+      // look-back warps take alternate stages, so in reproducible mode each
+      // gets a marker of its own (the later ones straight on `aggr`).
+      const int markers = P->reproducible ? kLookbackWarps : 1;
+      for (int e = 0; e < markers; ++e) {
+        const uint32_t ie = it + (uint32_t)e;
+        const int se = (int)(ie % kStages);
+        if (e > 0 && ie >= (uint32_t)kStages)
+          wait_empty_producer(&empty[se], (ie / kStages - 1) & 1u);
+        if (lane == 0) {
+          meta[se].kind = KIND_DONE;
+          meta[se].k = (uint32_t)e;
+          mbar_arrive(e == 0 ? &full[se] : &aggr[se]);
+        }
       }
+      return;
     }
     const uint32_t t = c.t;
     StageMeta &m = meta[s];
@@ -150,13 +145,6 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
         if (PAY) bulk_load(dp + (a0 - tstart), psrc + a0, (uint32_t)((a1 - a0) * 4), &full[s]);
       } else {
         mbar_arrive(&full[s]);
-      }
-    }
-    if (ahead) {
-      c = claim_tile(P, cur, ctl, ntiles);
-      if (c.t >= ntiles) {
-        if (lane == 0) *done_iter = it + 1;
-        return;
       }
     }
   }
@@ -222,8 +210,7 @@ __device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long lon
 }
 
 __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
-                                              StageMeta *meta, int lw,
-                                              const volatile uint32_t *done_iter) {
+                                              StageMeta *meta, int lw) {
   if (!P->reproducible) return;  // the counter warps reserve ranges instead
   const int lane = threadIdx.x & 31;
   u64 *lb = P->lookback[cur];
@@ -233,8 +220,15 @@ __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *agg
   // slow walk back delays only its own tiles
   for (uint32_t it = (uint32_t)lw;; it += kLookbackWarps) {
     const int s = (int)(it % kStages);
-    if (!wait_or_done(&aggr[s], (it / kStages) & 1u, done_iter, it)) return;
+    wait_aggr_lookback(&aggr[s], (it / kStages) & 1u);
     StageMeta &m = meta[s];
+    if (m.kind == KIND_DONE) {
+      // the first marker goes on to the consumers; later ones only stop
+      // the other look-back warps
+      __syncwarp();
+      if (lane == 0 && m.k == 0) mbar_arrive(&ready[s]);
+      return;
+    }
     const uint32_t t = m.t;
     if (m.kind == KIND_PARTITION && m.k > 0) {
       const u64 agg = m.agg;
