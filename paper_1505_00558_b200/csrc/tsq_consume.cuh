@@ -130,7 +130,7 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
     }
     const uint32_t t = m.t;
     if (lane == 0 && cw == 0) TSQ_MARK(level, t, 2);
-    const U *sk = in_k + (size_t)s * G::TILE;
+    const U *sk = in_k + (size_t)s * G::SLOT;
     const bool raw = P->raw[m.buf] != 0;
     const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
     const bool part = m.kind == KIND_PARTITION;
@@ -244,12 +244,26 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
   }
 }
 
-// Stage one consumer thread's keys of a tile into the out buffer: each key
-// goes to the thread's next < slot (counting up) or next > slot (counting
-// down); records also stage the == payloads.  MODE 0: both buffers hold
-// encoded keys, 1: source raw, 2: destination raw, 3: both raw.
+// One consumer thread's keys (and payloads) of a stage, into registers.
+template <class C, bool PAY>
+__device__ __forceinline__ void load_keys(const typename C::U *sk, const uint32_t *sp, int tid,
+                                          typename C::U *key, uint32_t *pay) {
+  typedef typename C::U U;
+  typedef Geo<C, PAY> G;
+#pragma unroll
+  for (int v = 0; v < G::VPT; ++v) {
+    const int e0 = (v * kConsumers + tid) * G::VN;
+    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key + v * G::VN);
+    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay + v * G::VN);
+  }
+}
+
+// Stage one consumer thread's keys back into the stage, in output order:
+// each key goes to the thread's next < slot (counting up) or next > slot
+// (counting down); records also stage the == payloads.  MODE 0: both
+// buffers hold encoded keys, 1: source raw, 2: destination raw, 3: both raw.
 template <class C, bool PAY, bool FULL, int MODE>
-__device__ __forceinline__ void stage_keys(const typename C::U *sk, const uint32_t *sp, int tid,
+__device__ __forceinline__ void stage_keys(const typename C::U *key, const uint32_t *pay, int tid,
                                            typename C::U piv, int rlo, int rhi, uint32_t plt,
                                            uint32_t pgt, uint32_t peq, typename C::U *ok,
                                            uint32_t *op) {
@@ -258,20 +272,17 @@ __device__ __forceinline__ void stage_keys(const typename C::U *sk, const uint32
 #pragma unroll
   for (int v = 0; v < G::VPT; ++v) {
     const int e0 = (v * kConsumers + tid) * G::VN;
-    U key[G::VN];
-    uint32_t pay[G::VN];
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
-    if (PAY) unpack(*reinterpret_cast<const typename Vec<U>::P *>(sp + e0), pay);
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) {
-      const U x = (MODE & 1) ? C::enc(key[q]) : key[q];
-      const U y = MODE == 2 ? C::dec(key[q]) : (MODE == 1 ? x : key[q]);
+      const U kq = key[v * G::VN + q];
+      const U x = (MODE & 1) ? C::enc(kq) : kq;
+      const U y = MODE == 2 ? C::dec(kq) : (MODE == 1 ? x : kq);
       const bool valid = FULL || (e0 + q >= rlo && e0 + q < rhi);
       const bool is_lt = valid && x < piv, is_gt = valid && x > piv;
       if (PAY) {
         const uint32_t pos = is_lt ? plt : (is_gt ? pgt : peq);
         if (is_lt || is_gt) ok[pos] = y;
-        if (valid) op[pos] = pay[q];
+        if (valid) op[pos] = pay[v * G::VN + q];
         peq += (valid && !is_lt && !is_gt) ? 1u : 0u;
       } else {
         const uint32_t pos = is_lt ? plt : pgt;
@@ -283,28 +294,36 @@ __device__ __forceinline__ void stage_keys(const typename C::U *sk, const uint32
   }
 }
 
-// Emit one tile: offsets from the look-back warp, ranks, staging, bulk
-// stores.  `ok` / `op` alternate between two buffers by tile parity.
+// Emit one tile: its offsets (reserved by the counters or resolved by the
+// look-back), every consumer's keys into registers, then -- once all are
+// loaded -- back into the same stage in output order, aligned like their
+// destinations, and out with bulk stores.  The stage goes back to the
+// producer once those stores have read it: thread 0 releases the previous
+// tile's stage after committing this one's (`pend`).
 template <class C, bool PAY>
-__device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const typename C::U *in_k,
-                                          const uint32_t *in_p, u64 *empty, StageMeta *meta,
-                                          const StageCounts *sc, typename C::U *ok, uint32_t *op) {
+__device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename C::U *in_k,
+                                          uint32_t *in_p, u64 *empty, StageMeta *meta,
+                                          const StageCounts *sc, int &pend) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
+  const int warp = tid >> 5;
   const int s = (int)(it % kStages);
   const StageMeta &m = meta[s];
   const uint32_t level = P->ctl->level;
   (void)level;
   if (m.kind != KIND_PARTITION) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0) mbar_arrive(&empty[s]);  // verified by the counters: nothing to write
     return;
   }
   const uint32_t t = m.t;
   (void)t;
   if (tid == 0) TSQ_MARK(level, t, 6);
+  U *sk = in_k + (size_t)s * G::SLOT;
+  uint32_t *sp = PAY ? in_p + (size_t)s * G::SLOT : nullptr;
+  U key[G::IPT];
+  uint32_t pay[G::IPT];
+  load_keys<C, PAY>(sk, sp, tid, key, pay);
   const StageCounts &c = sc[s];
   uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
 #pragma unroll
@@ -327,8 +346,6 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const ty
   const int o_gt = g_base + (int)(D_gt & (kAlign - 1));
   const int e_base = (o_gt + (int)t_gt + kAlign - 1) & ~(kAlign - 1);
   const int o_eq = e_base + (int)(D_eq & (kAlign - 1));
-  const U *sk = in_k + (size_t)s * G::TILE;
-  const uint32_t *sp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
   const U piv = (U)m.pivot;
   const int rlo = (int)(lo - m.tstart), rhi = (int)(m.hi - m.tstart);
   // this thread's first slots: warp offset + the counter's per-lane prefix
@@ -338,57 +355,62 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, const ty
   uint32_t pgt = (uint32_t)o_gt + t_gt - 1u - w_gt - e_gt;  // next > slot (backwards)
   uint32_t peq = (uint32_t)o_eq + w_eq + (e_va - e_lt - e_gt);
   const bool full = rlo == 0 && rhi == G::TILE;
+  named_sync(1, kConsumers);  // every consumer holds its keys: restage in place
   if (src_raw && dst_raw) {
-    if (full) stage_keys<C, PAY, true, 3>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
-    else stage_keys<C, PAY, false, 3>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    if (full) stage_keys<C, PAY, true, 3>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    else stage_keys<C, PAY, false, 3>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
   } else if (src_raw) {
-    if (full) stage_keys<C, PAY, true, 1>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
-    else stage_keys<C, PAY, false, 1>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    if (full) stage_keys<C, PAY, true, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    else stage_keys<C, PAY, false, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
   } else if (dst_raw) {
-    if (full) stage_keys<C, PAY, true, 2>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
-    else stage_keys<C, PAY, false, 2>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    if (full) stage_keys<C, PAY, true, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    else stage_keys<C, PAY, false, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
   } else {
-    if (full) stage_keys<C, PAY, true, 0>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
-    else stage_keys<C, PAY, false, 0>(sk, sp, tid, piv, rlo, rhi, plt, pgt, peq, ok, op);
+    if (full) stage_keys<C, PAY, true, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    else stage_keys<C, PAY, false, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
   }
-  // the stage is no longer needed: hand it back to the producer
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&empty[s]);
   fence_proxy_async_smem();
-  // the previous tile's bulk stores must be done reading the other out
-  // buffer before the next tile restages it (after this barrier)
-  if (tid == 0) bulk_wait_read0();
   named_sync(1, kConsumers);
   U *dst = reinterpret_cast<U *>(P->keys[db]);
   const bool issuer = tid == 0;
-  emit_run<U>(dst, D_lt, t_lt, ok, issuer, 1);
-  emit_run<U>(dst, D_gt, t_gt, ok + g_base, issuer, 2);
+  emit_run<U>(dst, D_lt, t_lt, sk, issuer, 1);
+  emit_run<U>(dst, D_gt, t_gt, sk + g_base, issuer, 2);
   if (PAY) {
     uint32_t *dpay = P->pay[db];
-    emit_run<uint32_t>(dpay, D_lt, t_lt, op, issuer, 3);
-    emit_run<uint32_t>(dpay, D_gt, t_gt, op + g_base, issuer, 4);
-    emit_run<uint32_t>(P->side_pay, D_eq, t_eq, op + e_base, issuer, 5);
+    emit_run<uint32_t>(dpay, D_lt, t_lt, sp, issuer, 3);
+    emit_run<uint32_t>(dpay, D_gt, t_gt, sp + g_base, issuer, 4);
+    emit_run<uint32_t>(P->side_pay, D_eq, t_eq, sp + e_base, issuer, 5);
   }
   if (issuer) {
     bulk_commit();
     TSQ_MARK(level, t, 7);
+    // the previous tile's stores have read their stage: hand it back
+    bulk_wait_read1();
+    if (pend >= 0) mbar_arrive(&empty[pend]);
+    pend = s;
   }
 }
 
 template <class C, bool PAY>
-__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ P) {
+__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ Pg) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
+  // every role reads the launch parameters per tile: keep a copy on chip
+  // (the global copy misses L1, which the shared-memory carve-out squeezes)
+  __shared__ __align__(16) Params sparams;
+  static_assert(sizeof(Params) % 8 == 0, "Params copy granularity");
+  if (threadIdx.x < sizeof(Params) / 8)
+    reinterpret_cast<u64 *>(&sparams)[threadIdx.x] = reinterpret_cast<const u64 *>(Pg)[threadIdx.x];
+  const Params *P = &sparams;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   U *in_k = reinterpret_cast<U *>(smem_raw);
-  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)kStages * G::TILE);
-  unsigned char *outb = smem_raw + (size_t)kStages * G::STAGE_BYTES;
+  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)kStages * G::SLOT);
   __shared__ __align__(8) u64 full[kStages], aggr[kStages], ready[kStages], empty[kStages];
   __shared__ StageMeta meta[kStages];
   __shared__ StageCounts sc[kStages];
   __shared__ CounterShare cshare[kStages];
 
-  Ctl *ctl = P->ctl;
+  Ctl *ctl = Pg->ctl;  // (the on-chip copy is complete after the barrier below)
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u);
   const uint32_t ntiles = ctl->cur_ntiles;
@@ -398,7 +420,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
       mbar_init(&full[s], 1);
       mbar_init(&aggr[s], 1);
       mbar_init(&ready[s], 1);
-      mbar_init(&empty[s], kConsumerWarps + kCounterWarps);  // consumers + counters
+      mbar_init(&empty[s], 1 + kCounterWarps);  // consumers (thread 0) + counters
     }
     fence_barrier_init();
   }
@@ -417,15 +439,17 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
     lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp);
     return;
   }
+  int pend = -1;  // (thread 0) the stage the last bulk stores may still be reading
   for (uint32_t k = 0;; ++k) {
     const int s = (int)(k % kStages);
     wait_ready_consumer(&ready[s], (k / kStages) & 1u);
     if (meta[s].kind == KIND_DONE) break;
-    unsigned char *ob = outb + (size_t)(k & 1u) * (G::OUT_K + G::OUT_P);
-    emit_tile<C, PAY>(P, k, in_k, in_p, empty, meta, sc, reinterpret_cast<U *>(ob),
-                      reinterpret_cast<uint32_t *>(ob + G::OUT_K));
+    emit_tile<C, PAY>(P, k, in_k, in_p, empty, meta, sc, pend);
   }
-  if (threadIdx.x == 0) bulk_wait0();
+  if (threadIdx.x == 0) {
+    bulk_wait0();
+    if (pend >= 0) mbar_arrive(&empty[pend]);
+  }
 }
 
 }  // namespace tsq

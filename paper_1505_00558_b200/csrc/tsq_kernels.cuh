@@ -42,9 +42,9 @@ constexpr int kLookbackWarps = 2;                 // alternate stages between th
 constexpr int kCounterWarp = kLookbackWarp + kLookbackWarps;  // warps 11-14: counts
 constexpr int kCounterWarps = 4;
 constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps + kCounterWarps);
-constexpr int kStages = 4;                        // input ring depth
+constexpr int kStages = 6;                        // stage ring depth
 constexpr int kAlign = 4;                         // bulk-copy element alignment
-constexpr int kOutPad = 16;                       // alignment slack of the out buffer
+constexpr int kOutPad = 16;                       // alignment slack of a restaged tile
 constexpr uint32_t kDone = 0xffffffffu;
 
 template <class C, bool PAY>
@@ -54,11 +54,12 @@ struct Geo {
   static constexpr int VPT = 4;            // vectors per thread per tile
   static constexpr int IPT = VN * VPT;     // keys per thread per tile
   static constexpr int TILE = kConsumers * IPT;
+  // a stage holds a tile as loaded and then, restaged in place, its output
+  // runs, each aligned like its destination (<= 3 slots of padding per run)
+  static constexpr int SLOT = TILE + kOutPad;
   static constexpr size_t KB = sizeof(U);
-  static constexpr size_t STAGE_BYTES = (size_t)TILE * (KB + (PAY ? 4 : 0));
-  static constexpr size_t OUT_K = (size_t)(TILE + kOutPad) * KB;
-  static constexpr size_t OUT_P = PAY ? (size_t)(TILE + kOutPad) * 4 : 0;
-  static constexpr size_t SMEM = (size_t)kStages * STAGE_BYTES + 2 * (OUT_K + OUT_P);
+  static constexpr size_t STAGE_BYTES = (size_t)SLOT * (KB + (PAY ? 4 : 0));
+  static constexpr size_t SMEM = (size_t)kStages * STAGE_BYTES;
 };
 
 __device__ __forceinline__ void unpack(const uint4 &v, uint32_t *o) {

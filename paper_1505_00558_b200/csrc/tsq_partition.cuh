@@ -27,6 +27,10 @@
 // complete in, so the consumers rarely wait for offsets.
 #pragma once
 
+#ifndef TSQ_CLAIM_AHEAD
+#define TSQ_CLAIM_AHEAD 1
+#endif
+
 namespace tsq {
 
 // ---------------------------------------------------------------------------
@@ -64,13 +68,18 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
   Ctl *ctl = P->ctl;
   const uint32_t level = ctl->level;
   (void)level;
-  // a tile is claimed only once a stage is free for it, so claim order
-  // tracks processing order across CTAs (a look-back waits on predecessors)
+  // Reservation mode claims (and resolves) the next tile right after
+  // issuing a load, so the claim's round trips overlap the wait for a free
+  // stage.  Look-back mode claims only once a stage is free, so claim order
+  // tracks processing order across CTAs (a look-back waits on predecessors).
+  const bool ahead = TSQ_CLAIM_AHEAD && !P->reproducible;
+  Claim nx;
+  if (ahead) nx = claim_tile(P, cur, ctl, ntiles);
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
     const uint32_t j = it / kStages;
     if (j > 0) wait_empty_producer(&empty[s], (j - 1) & 1u);
-    const Claim c = claim_tile(P, cur, ctl, ntiles);
+    const Claim c = ahead ? nx : claim_tile(P, cur, ctl, ntiles);
     if (c.t >= ntiles) {
       // out of tiles: a DONE marker in the next stage stops every role.  The
       // look-back warps take alternate stages, so in reproducible mode each
@@ -102,8 +111,8 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
     const uint32_t *psrc = PAY ? P->pay[buf] : nullptr;
     uint32_t skip = 0;
     if (kind != KIND_PARTITION) skip = ld_volatile32(&P->segs[cur][c.sid].fail) != 0 ? 1u : 0u;
-    U *dk = in_k + (size_t)s * G::TILE;
-    uint32_t *dp = PAY ? in_p + (size_t)s * G::TILE : nullptr;
+    U *dk = in_k + (size_t)s * G::SLOT;
+    uint32_t *dp = PAY ? in_p + (size_t)s * G::SLOT : nullptr;
     uint32_t tx = 0;
     long long a0 = 0, a1 = 0;
     if (!skip) {
@@ -147,6 +156,7 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
         mbar_arrive(&full[s]);
       }
     }
+    if (ahead) nx = claim_tile(P, cur, ctl, ntiles);
   }
 }
 
