@@ -99,13 +99,13 @@ struct CounterShare {
 // Counter warps: all kCounterWarps warps take every tile, warp cw counting
 // the slices of consumer warps [cw * kSlices, (cw + 1) * kSlices) -- a tile
 // is counted in a quarter of the time one warp would take.  The warp that
-// finishes a tile last combines the shares and either reserves the tile's
-// output ranges with one atomic (default) or publishes its aggregate for
-// the look-back warps (reproducible mode).
+// finishes a tile last combines the shares into the tile's aggregate (and
+// in reproducible mode publishes it for the decoupled look-back) and hands
+// the stage to the look-back warps, which turn it into the tile's offsets.
 template <class C, bool PAY>
 __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typename C::U *in_k,
-                                             u64 *full, u64 *aggr, u64 *ready, u64 *empty,
-                                             StageMeta *meta, StageCounts *sc, CounterShare *cs,
+                                             u64 *full, u64 *aggr, u64 *empty, StageMeta *meta,
+                                             StageCounts *sc, CounterShare *cs,
                                              int cw) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
@@ -123,8 +123,7 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
-        if (atomicAdd(&cs[s].finished, 1u) == kCounterWarps - 1)
-          mbar_arrive(reproducible ? &aggr[s] : &ready[s]);
+        if (atomicAdd(&cs[s].finished, 1u) == kCounterWarps - 1) mbar_arrive(&aggr[s]);
       }
       return;
     }
@@ -141,14 +140,14 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       if (!m.skip) {
         const bool asc = m.kind == KIND_VERIFY_ASC;
         for (int i = rlo + cw * 32 + lane; i < rhi; i += 32 * kCounterWarps) {
-          U a = sk[i], b;
+          U a = sk[i], b = a;
           bool have = true;
           if (i + 1 < rhi) b = sk[i + 1];
-          else if (m.has_next) b = (U)m.next_key;
+          else if (m.has_next) b = reinterpret_cast<const U *>(P->keys[m.buf])[m.hi];
           else have = false;
           if (raw) {
             a = C::enc(a);
-            if (i + 1 < rhi) b = C::enc(b);
+            b = C::enc(b);
           }
           if (have) bad |= asc ? (a > b) : (a < b);
         }
@@ -220,24 +219,13 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
           }
           const u64 agg = ((u64)tl << 31) | (u64)tg;
           m.agg = agg;
-          if (reproducible) {
+          m.eq_excl = tv - tl - tg;  // (the look-back warp turns it into a slot)
+          if (reproducible)
             st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
-          } else {
-            // reserve the tile's < and > ranges of its segment in one atomic
-            // on the segment's fill word (first tile's descriptor slot)
-            const u64 ex = atomicAdd(reinterpret_cast<unsigned long long *>(
-                                         &P->lookback[cur][m.tile_base]), agg);
-            const uint32_t eqx =
-                PAY ? atomicAdd(&P->segs[cur][m.sid].eq_fill, tv - tl - tg) : 0u;
-            m.excl = ex;
-            m.eq_excl = eqx;
-            TSQ_MARK(level, t, 4);
-          }
           TSQ_MARK(level, t, 3);
         }
-        // reproducible: the look-back warp resolves the offsets; otherwise
-        // the reservation above did and the consumers may go
-        mbar_arrive(reproducible ? &aggr[s] : &ready[s]);
+        // the look-back warps turn the aggregate into the tile's offsets
+        mbar_arrive(&aggr[s]);
       }
       mbar_arrive(&empty[s]);  // done reading the stage
     }
@@ -356,6 +344,20 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   uint32_t peq = (uint32_t)o_eq + w_eq + (e_va - e_lt - e_gt);
   const bool full = rlo == 0 && rhi == G::TILE;
   named_sync(1, kConsumers);  // every consumer holds its keys: restage in place
+#if defined(TSQ_EXP_COPY) && !defined(TSQ_EXP_STAGE)
+  if (full) {  // experiment: pipeline ceiling -- the tile goes out unpartitioned
+    fence_proxy_async_smem();
+    named_sync(1, kConsumers);
+    if (tid == 0) {
+      bulk_store(reinterpret_cast<U *>(P->keys[db]) + m.tstart, sk, G::TILE * sizeof(U));
+      bulk_commit();
+      bulk_wait_read1();
+      if (pend >= 0) mbar_arrive(&empty[pend]);
+      pend = s;
+    }
+    return;
+  }
+#endif
   if (src_raw && dst_raw) {
     if (full) stage_keys<C, PAY, true, 3>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
     else stage_keys<C, PAY, false, 3>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
@@ -371,6 +373,18 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   }
   fence_proxy_async_smem();
   named_sync(1, kConsumers);
+#ifdef TSQ_EXP_STAGE
+  if (full) {  // experiment: restaged, then out as one contiguous store
+    if (tid == 0) {
+      bulk_store(reinterpret_cast<U *>(P->keys[db]) + m.tstart, sk, G::TILE * sizeof(U));
+      bulk_commit();
+      bulk_wait_read1();
+      if (pend >= 0) mbar_arrive(&empty[pend]);
+      pend = s;
+    }
+    return;
+  }
+#endif
   U *dst = reinterpret_cast<U *>(P->keys[db]);
   const bool issuer = tid == 0;
   emit_run<U>(dst, D_lt, t_lt, sk, issuer, 1);
@@ -431,12 +445,12 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
     return;
   }
   if (warp >= kCounterWarp) {
-    counter_loop<C, PAY>(P, cur, in_k, full, aggr, ready, empty, meta, sc, cshare,
+    counter_loop<C, PAY>(P, cur, in_k, full, aggr, empty, meta, sc, cshare,
                          warp - kCounterWarp);
     return;
   }
   if (warp >= kLookbackWarp) {
-    lookback_loop(P, cur, aggr, ready, meta, warp - kLookbackWarp);
+    lookback_loop<PAY>(P, cur, aggr, ready, meta, warp - kLookbackWarp);
     return;
   }
   int pend = -1;  // (thread 0) the stage the last bulk stores may still be reading

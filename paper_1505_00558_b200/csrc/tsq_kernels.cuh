@@ -77,7 +77,7 @@ __device__ __forceinline__ void unpack(const uint2 &v, uint32_t *o) {
 // `excl` (its exclusive prefix in its segment) by the look-back warp.
 struct StageMeta {
   long long tstart, lo, hi, begin, end;
-  u64 pivot, next_key, agg, excl;
+  u64 pivot, agg, excl;
   uint32_t t, k, kind, buf, tile_base, sid, skip, has_next;
   uint32_t eq_excl;  // records, atomic placement: this tile's first == side slot
 };

@@ -27,37 +27,45 @@
 // complete in, so the consumers rarely wait for offsets.
 #pragma once
 
-#ifndef TSQ_CLAIM_AHEAD
-#define TSQ_CLAIM_AHEAD 1
-#endif
-
 namespace tsq {
 
 // ---------------------------------------------------------------------------
 // Producer warp.
 
-// A claimed tile and the fields of its segment the producer needs.
-struct Claim {
-  uint32_t t, sid, tile_base, kind, buf;
+// The fields of a tile's segment the producer needs, resolved for a batch
+// of 32 upcoming tiles at a time (one per lane) so their dependent global
+// loads overlap instead of serialising the producer tile by tile.
+struct TileSeg {
   long long begin, end;
   u64 pivot;
+  uint32_t sid, tile_base, kind, buf, fail;
 };
 
-__device__ __forceinline__ Claim claim_tile(const Params *P, int cur, Ctl *ctl, uint32_t ntiles) {
-  const int lane = threadIdx.x & 31;
-  Claim c;
-  uint32_t t = 0;
-  if (lane == 0) t = atomicAdd(&ctl->tile_ticket, 1u);
-  c.t = __shfl_sync(0xffffffffu, t, 0);
-  if (c.t >= ntiles) return c;
-  c.sid = P->tilemap[cur][c.t];
-  const Seg *sgp = &P->segs[cur][c.sid];
-  c.begin = sgp->begin; c.end = sgp->end;
-  c.tile_base = sgp->tile_base; c.kind = sgp->kind; c.buf = sgp->buf;
-  c.pivot = sgp->pivot;
-  return c;
+__device__ __forceinline__ TileSeg resolve_tile(const Params *P, int cur, uint32_t t,
+                                                uint32_t ntiles) {
+  TileSeg r;
+  r.begin = r.end = 0; r.pivot = 0; r.sid = r.tile_base = r.kind = r.buf = r.fail = 0;
+  if (t < ntiles) {
+    r.sid = P->tilemap[cur][t];
+    const Seg *sg = &P->segs[cur][r.sid];
+    r.begin = sg->begin; r.end = sg->end; r.pivot = sg->pivot;
+    r.tile_base = sg->tile_base; r.kind = sg->kind; r.buf = sg->buf;
+    // a verification that already failed elsewhere needs no more data (a
+    // hint: a stale 0 only costs the load)
+    r.fail = r.kind != KIND_PARTITION ? ld_volatile32(&sg->fail) : 0u;
+  }
+  return r;
 }
 
+template <typename T>
+__device__ __forceinline__ T bcast(T v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+// Tiles are dealt round-robin: CTA b takes tiles b, b + G, b + 2G, ...  of
+// the level (G = persistent grid size), so processing order follows tile
+// order across CTAs (a look-back waits on its predecessors) and no claim
+// sits on the producer's critical path.
 template <class C, bool PAY>
 __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t ntiles,
                                               typename C::U *in_k, uint32_t *in_p, u64 *full,
@@ -65,26 +73,24 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   const int lane = threadIdx.x & 31;
-  Ctl *ctl = P->ctl;
-  const uint32_t level = ctl->level;
+  const uint32_t level = P->ctl->level;
   (void)level;
-  // Reservation mode claims (and resolves) the next tile right after
-  // issuing a load, so the claim's round trips overlap the wait for a free
-  // stage.  Look-back mode claims only once a stage is free, so claim order
-  // tracks processing order across CTAs (a look-back waits on predecessors).
-  const bool ahead = TSQ_CLAIM_AHEAD && !P->reproducible;
-  Claim nx;
-  if (ahead) nx = claim_tile(P, cur, ctl, ntiles);
+  const u64 grid = gridDim.x;
+  TileSeg mine;  // lane j: the tile of iteration (it & ~31) + j
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % kStages);
     const uint32_t j = it / kStages;
+    const u64 t64 = blockIdx.x + (u64)it * grid;
+    if ((it & 31u) == 0) {
+      const u64 tl = blockIdx.x + (u64)(it + lane) * grid;
+      mine = resolve_tile(P, cur, tl < ntiles ? (uint32_t)tl : ntiles, ntiles);
+    }
     if (j > 0) wait_empty_producer(&empty[s], (j - 1) & 1u);
-    const Claim c = ahead ? nx : claim_tile(P, cur, ctl, ntiles);
-    if (c.t >= ntiles) {
+    if (t64 >= ntiles) {
       // out of tiles: a DONE marker in the next stage stops every role.  The
-      // look-back warps take alternate stages, so in reproducible mode each
-      // gets a marker of its own (the later ones straight on `aggr`).
-      const int markers = P->reproducible ? kLookbackWarps : 1;
+      // look-back warps take alternate stages, so each gets a marker of its
+      // own (the later ones straight on `aggr`).
+      const int markers = kLookbackWarps;
       for (int e = 0; e < markers; ++e) {
         const uint32_t ie = it + (uint32_t)e;
         const int se = (int)(ie % kStages);
@@ -98,19 +104,21 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
       }
       return;
     }
-    const uint32_t t = c.t;
+    const uint32_t t = (uint32_t)t64;
+    const int src_lane = (int)(it & 31u);
+    const long long begin = bcast(mine.begin, src_lane), end = bcast(mine.end, src_lane);
+    const u64 pivot = bcast(mine.pivot, src_lane);
+    const uint32_t sid = bcast(mine.sid, src_lane), tile_base = bcast(mine.tile_base, src_lane);
+    const uint32_t kind = bcast(mine.kind, src_lane), buf = bcast(mine.buf, src_lane);
+    const uint32_t skip = bcast(mine.fail, src_lane) != 0 ? 1u : 0u;
     StageMeta &m = meta[s];
     TSQ_MARK(level, t, 0);
-    const long long begin = c.begin, end = c.end;
-    const uint32_t kind = c.kind, buf = c.buf;
-    const uint32_t k = t - c.tile_base;
+    const uint32_t k = t - tile_base;
     const long long tstart = (begin / G::TILE + k) * (long long)G::TILE;
     const long long lo = tstart > begin ? tstart : begin;
     const long long hi = (tstart + G::TILE) < end ? (tstart + G::TILE) : end;
     const U *src = reinterpret_cast<const U *>(P->keys[buf]);
     const uint32_t *psrc = PAY ? P->pay[buf] : nullptr;
-    uint32_t skip = 0;
-    if (kind != KIND_PARTITION) skip = ld_volatile32(&P->segs[cur][c.sid].fail) != 0 ? 1u : 0u;
     U *dk = in_k + (size_t)s * G::SLOT;
     uint32_t *dp = PAY ? in_p + (size_t)s * G::SLOT : nullptr;
     uint32_t tx = 0;
@@ -137,16 +145,10 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
     __syncwarp();
     if (lane == 0) {
       m.tstart = tstart; m.lo = lo; m.hi = hi; m.begin = begin; m.end = end;
-      m.pivot = c.pivot;
-      m.t = t; m.k = k; m.kind = kind; m.buf = buf; m.tile_base = c.tile_base; m.sid = c.sid;
+      m.pivot = pivot;
+      m.t = t; m.k = k; m.kind = kind; m.buf = buf; m.tile_base = tile_base; m.sid = sid;
       m.skip = skip;
-      m.has_next = 0;
-      if (kind != KIND_PARTITION && !skip && hi < end) {
-        U v = src[hi];
-        if (P->raw[buf]) v = C::enc(v);
-        m.next_key = (u64)v;
-        m.has_next = 1;
-      }
+      m.has_next = hi < end ? 1u : 0u;  // verification: the counters read key hi
       TSQ_MARK(level, t, 1);
       if (tx) {
         mbar_arrive_expect_tx(&full[s], tx);
@@ -156,7 +158,6 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
         mbar_arrive(&full[s]);
       }
     }
-    if (ahead) nx = claim_tile(P, cur, ctl, ntiles);
   }
 }
 
@@ -219,15 +220,20 @@ __device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long lon
   }
 }
 
+// Look-back warps: take alternate stages once counted and give each tile its
+// offsets in its segment -- by decoupled look-back over the segment's earlier
+// tiles (reproducible mode), or by reserving its < and > ranges with one
+// atomic on the segment's fill word (the first tile's descriptor slot; the
+// records' == payload slots on the segment's eq_fill).  Either way the
+// counters never wait on a global round trip.
+template <bool PAY>
 __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
                                               StageMeta *meta, int lw) {
-  if (!P->reproducible) return;  // the counter warps reserve ranges instead
   const int lane = threadIdx.x & 31;
   u64 *lb = P->lookback[cur];
+  const bool reproducible = P->reproducible != 0;
   const uint32_t level = P->ctl->level;
   (void)level;
-  // look-back warp lw owns every kLookbackWarps-th tile of this CTA, so a
-  // slow walk back delays only its own tiles
   for (uint32_t it = (uint32_t)lw;; it += kLookbackWarps) {
     const int s = (int)(it % kStages);
     wait_aggr_lookback(&aggr[s], (it / kStages) & 1u);
@@ -240,7 +246,18 @@ __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *agg
       return;
     }
     const uint32_t t = m.t;
-    if (m.kind == KIND_PARTITION && m.k > 0) {
+    (void)t;
+    if (m.kind != KIND_PARTITION) {
+      // verified by the counters: nothing to place
+    } else if (!reproducible) {
+      if (lane == 0) {
+        const u64 ex = atomicAdd(reinterpret_cast<unsigned long long *>(&lb[m.tile_base]), m.agg);
+        const uint32_t eqx = PAY ? atomicAdd(&P->segs[cur][m.sid].eq_fill, m.eq_excl) : 0u;
+        m.excl = ex;
+        m.eq_excl = eqx;
+        TSQ_MARK(level, t, 4);
+      }
+    } else if (m.k > 0) {
       const u64 agg = m.agg;
       const u64 excl = lookback_window(lb, (long long)t - 1, (long long)m.tile_base);
       if (lane == 0) {
