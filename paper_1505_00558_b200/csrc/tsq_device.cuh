@@ -224,27 +224,47 @@ __device__ __forceinline__ void mbar_wait(u64 *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// distinct copies per wait site so profiles attribute stalls to the role
-#define TSQ_WAIT_ASM                                                              \
-  "{\n\t.reg .pred p;\n\tTSQ_W_%=:\n\t"                                         \
-  "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t@!p bra TSQ_W_%=;\n\t}"
-__device__ __forceinline__ void wait_full_consumer(u64 *bar, uint32_t parity) {
+// Waits: probe the barrier; while it is not there yet, back off with a
+// short sleep.  (The suspend hint of try_wait alone wakes on every barrier
+// event of the CTA, so idle warps would spin and take issue slots from the
+// working ones.)  Distinct copies per role so profiles attribute the waits.
+#ifndef TSQ_SLEEP_NS
+#define TSQ_SLEEP_NS 32
+#endif
+#ifndef TSQ_SLEEP_PRODUCER_NS
+#define TSQ_SLEEP_PRODUCER_NS 64
+#endif
+__device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+template <int NS>
+__device__ __forceinline__ void mbar_wait_sleep(u64 *bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+  while (!mbar_test(a, parity)) {
+    if (NS > 0) __nanosleep(NS);
+  }
+}
+__device__ __forceinline__ void wait_full_consumer(u64 *bar, uint32_t parity) {
+  mbar_wait_sleep<TSQ_SLEEP_NS>(bar, parity);
 }
 __device__ __forceinline__ void wait_aggr_lookback(u64 *bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+  mbar_wait_sleep<TSQ_SLEEP_NS>(bar, parity);
 }
 __device__ __forceinline__ void wait_ready_consumer(u64 *bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+  mbar_wait_sleep<TSQ_SLEEP_NS>(bar, parity);
 }
 __device__ __forceinline__ void wait_empty_producer(u64 *bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  asm volatile(TSQ_WAIT_ASM ::"r"(a), "r"(parity) : "memory");
+  mbar_wait_sleep<TSQ_SLEEP_PRODUCER_NS>(bar, parity);
 }
-#undef TSQ_WAIT_ASM
+
 
 // 1-D bulk copy global -> shared, completing `bytes` on the mbarrier
 // (cp.async.bulk: SASS UBLKCP); dst/src 16-byte aligned, bytes % 16 == 0
