@@ -38,9 +38,12 @@ KernelSet make_set() {
   s.tile = Geo<C, PAY>::TILE;
   s.part_smem = Geo<C, PAY>::SMEM;
   s.sched_smem = (size_t)(kThreads / 32) * (kMaxSample + 1) * sizeof(U);
-  // keys + indices in padded rows of 17, staged payloads (see tsq_small.cuh)
-  s.small_smem = (size_t)kThreads * (kSmallT / kThreads + 1) * (sizeof(U) + (PAY ? 4 : 0)) +
-                 (PAY ? (size_t)kSmallT * 4 : 0);
+  // two padded-row merge buffers (+ index arrays), see tsq_small.cuh
+  {
+    typedef MergeTraits<Codec<DT>, PAY> M;
+    const size_t np = (size_t)kSmallT + (kSmallT >> kLogVT);
+    s.small_smem = 2 * np * sizeof(typename M::K) + (M::kIdx ? 2 * np * 4 : 0);
+  }
   return s;
 }
 

@@ -162,62 +162,260 @@ __device__ __forceinline__ void block_bitonic(SortItem<U, PAY> (&v)[E], U *xk, u
   }
 }
 
-template <class C, bool PAY, int E>
+// ---------------------------------------------------------------------------
+// The on-chip sort proper: every warp sorts 512 items (16 per lane) with a
+// bitonic network in registers and shuffles, then log2(len/512) rounds merge
+// pairs of sorted runs through shared memory along merge paths -- each
+// thread binary-searches where its 16 outputs start and merges them
+// sequentially.  Padding only to a multiple of 512 (merge runs are clamped to
+// the segment length).
+//
+// Sort item: keys only -> the key; records with 32-bit keys -> key << 32 |
+// local index in one u64; records with 64-bit keys -> (key, index) pairs in
+// two arrays.  The index breaks ties (every item distinct) and gathers the
+// payloads at the end.
+
+constexpr int kVT = 16;     // items per thread
+constexpr int kLogVT = 4;
+
+template <class C, bool PAY>
+struct MergeTraits {
+  typedef typename C::U U;
+  static constexpr bool kPack = PAY && sizeof(U) == 4;   // (key, index) in one u64
+  static constexpr bool kIdx = PAY && sizeof(U) == 8;    // separate index array
+  typedef typename std::conditional<kPack, u64, U>::type K;
+};
+
+__device__ __forceinline__ int pidx(int i) { return i + (i >> kLogVT); }  // padded rows
+
+template <typename K, bool IDX>
+__device__ __forceinline__ bool mless(K a, uint32_t ia, K b, uint32_t ib) {
+  return IDX ? (a < b || (a == b && ia < ib)) : a < b;
+}
+
+template <typename K, bool IDX>
+__device__ __forceinline__ void mcmpx(K &a, uint32_t &ia, K &b, uint32_t &ib) {
+  if (IDX) {
+    const bool sw = mless<K, IDX>(b, ib, a, ia);
+    const K x = a; const uint32_t ix = ia;
+    a = sw ? b : a; ia = sw ? ib : ia;
+    b = sw ? x : b; ib = sw ? ix : ib;
+  } else {
+    const K x = a, y = b;
+    a = x < y ? x : y;
+    b = x < y ? y : x;
+  }
+}
+
+// in-register bitonic sort of kVT items (all-ascending formulation)
+template <typename K, bool IDX>
+__device__ __forceinline__ void sort_thread(K (&v)[kVT], uint32_t (&vi)[kVT]) {
+#pragma unroll
+  for (int k = 2; k <= kVT; k <<= 1) {
+#pragma unroll
+    for (int r = 0; r < kVT; ++r) {
+      const int p = r ^ (k - 1);
+      if (r < p) mcmpx<K, IDX>(v[r], vi[r], v[p], vi[p]);
+    }
+#pragma unroll
+    for (int j = k >> 2; j >= 1; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < kVT; ++r)
+        if (!(r & j)) mcmpx<K, IDX>(v[r], vi[r], v[r | j], vi[r | j]);
+    }
+  }
+}
+
+template <typename K>
+__device__ __forceinline__ K shfl_xor_k(K v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+
+// x <- min(x, y) if keep_min else max(x, y)
+template <typename K, bool IDX>
+__device__ __forceinline__ void mkeep(K &x, uint32_t &ix, K y, uint32_t iy, bool keep_min) {
+  if (IDX) {
+    const bool take = mless<K, IDX>(y, iy, x, ix) == keep_min;
+    x = take ? y : x;
+    ix = take ? iy : ix;
+  } else {
+    const K mn = x < y ? x : y, mx = x < y ? y : x;
+    x = keep_min ? mn : mx;
+  }
+}
+
+// Bitonic sort of the warp's 32 * kVT items, lane l holding l*kVT ..
+// l*kVT + kVT - 1: in-thread merges first, then merges of 32 .. 32 kVT with
+// shuffle stages for the cross-lane strides.
+template <typename K, bool IDX>
+__device__ __forceinline__ void warp_sort(K (&v)[kVT], uint32_t (&vi)[kVT]) {
+  const int lane = threadIdx.x & 31;
+  sort_thread<K, IDX>(v, vi);
+#pragma unroll 1
+  for (int k = 2 * kVT; k <= 32 * kVT; k <<= 1) {
+    {
+      const int m = k / kVT - 1;
+      const bool lower = (lane & (k / (2 * kVT))) == 0;
+      K y[kVT];
+      uint32_t yi[kVT];
+#pragma unroll
+      for (int r = 0; r < kVT; ++r) {
+        y[r] = shfl_xor_k<K>(v[kVT - 1 - r], m);
+        yi[r] = IDX ? __shfl_xor_sync(0xffffffffu, vi[kVT - 1 - r], m) : 0u;
+      }
+#pragma unroll
+      for (int r = 0; r < kVT; ++r) mkeep<K, IDX>(v[r], vi[r], y[r], yi[r], lower);
+    }
+#pragma unroll 1
+    for (int j = k >> 2; j >= kVT; j >>= 1) {
+      const int m = j / kVT;
+      const bool lower = (lane & m) == 0;
+#pragma unroll
+      for (int r = 0; r < kVT; ++r) {
+        const K y = shfl_xor_k<K>(v[r], m);
+        const uint32_t yi = IDX ? __shfl_xor_sync(0xffffffffu, vi[r], m) : 0u;
+        mkeep<K, IDX>(v[r], vi[r], y, yi, lower);
+      }
+    }
+#pragma unroll
+    for (int j = kVT / 2; j >= 1; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < kVT; ++r)
+        if (!(r & j)) mcmpx<K, IDX>(v[r], vi[r], v[r | j], vi[r | j]);
+    }
+  }
+}
+
+// One merge step for the thread whose outputs start at `o`: runs of length R
+// (clamped to len) in (S, SI), kVT outputs into registers.
+template <typename K, bool IDX>
+__device__ __forceinline__ int merge_thread(const K *S, const uint32_t *SI, int o, int R, int len,
+                                            K (&out)[kVT], uint32_t (&oi)[kVT]) {
+  const int base = o & ~(2 * R - 1);
+  const int a0 = base, na = min(R, len - base);
+  const int b0 = base + na, nb = max(0, min(R, len - base - R));
+  const int diag = o - base;
+  int lo = max(0, diag - nb), hi = min(diag, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const int pa = pidx(a0 + mid), pb = pidx(b0 + diag - 1 - mid);
+    const K ka = S[pa], kb = S[pb];
+    const uint32_t ja = IDX ? SI[pa] : 0u, jb = IDX ? SI[pb] : 0u;
+    if (mless<K, IDX>(kb, jb, ka, ja)) hi = mid;
+    else lo = mid + 1;
+  }
+  int ia = a0 + lo, ib = b0 + (diag - lo);
+  const int ae = a0 + na, be = b0 + nb;
+  // an exhausted run reads as the sentinel (greater than every item)
+  const K SENT = ~K(0);
+  K ka = ia < ae ? S[pidx(ia)] : SENT, kb = ib < be ? S[pidx(ib)] : SENT;
+  uint32_t ja = IDX ? (ia < ae ? SI[pidx(ia)] : 0xffffffffu) : 0u;
+  uint32_t jb = IDX ? (ib < be ? SI[pidx(ib)] : 0xffffffffu) : 0u;
+  const int cnt = min(kVT, na + nb - diag);
+#pragma unroll
+  for (int r = 0; r < kVT; ++r) {
+    const bool ta = !mless<K, IDX>(kb, jb, ka, ja);
+    out[r] = ta ? ka : kb;
+    if (IDX) oi[r] = ta ? ja : jb;
+    const int nx = ta ? ++ia : ++ib;
+    const bool ok = nx < (ta ? ae : be);
+    const K kn = ok ? S[pidx(nx)] : SENT;
+    const uint32_t jn = IDX ? (ok ? SI[pidx(nx)] : 0xffffffffu) : 0u;
+    if (ta) { ka = kn; ja = jn; } else { kb = kn; jb = jn; }
+  }
+  return cnt;
+}
+
+template <class C, bool PAY>
 __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &sm,
                                                unsigned char *smem) {
   typedef typename C::U U;
-  constexpr int N = kThreads * E;
-  constexpr int ROW = E + 1;  // padded row per thread for blocked access
-  // smem: keys [kThreads * ROW] | indices [kThreads * ROW] | payloads [N]
-  U *xk = reinterpret_cast<U *>(smem);
-  uint32_t *xi = reinterpret_cast<uint32_t *>(xk + kThreads * ROW);
-  uint32_t *sp = xi + (PAY ? kThreads * ROW : 0);
+  typedef MergeTraits<C, PAY> M;
+  typedef typename M::K K;
+  constexpr bool IDX = M::kIdx;
+  constexpr int NP = kSmallT + (kSmallT >> kLogVT);  // padded capacity
+  // smem: buffers A, B [NP] of K | (records, 64-bit keys) index A, B [NP]
+  K *ka = reinterpret_cast<K *>(smem), *kb = ka + NP;  // current / other buffer
+  uint32_t *ia = reinterpret_cast<uint32_t *>(kb + NP), *ib = ia + (IDX ? NP : 0);
   const int tid = threadIdx.x;
+  const int len = sm.len;
+  // threads holding items: whole warps (the warp sort covers 32 * kVT)
+  const int rows = ((len + 32 * kVT - 1) / (32 * kVT)) * 32;
   const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
   const bool raw = P->raw[sm.buf] != 0;
-  const int len = sm.len;
-  // coalesced load into padded rows: element i -> row i / E, column i % E
-  for (int i = tid; i < N; i += kThreads) {
-    U x = KeyMax<U>::v;
+  // coalesced load into padded rows (sentinels complete the last row)
+  for (int i = tid; i < rows * kVT; i += kThreads) {
+    K x;
+    uint32_t xi = 0xffffffffu;
     if (i < len) {
-      x = src[i];
-      if (raw) x = C::enc(x);
+      U k = src[i];
+      if (raw) k = C::enc(k);
+      xi = (uint32_t)i;
+      x = M::kPack ? (K)(((u64)k << 32) | (u64)i) : (K)k;
+    } else {
+      x = ~K(0);
     }
-    xk[(i / E) * ROW + (i % E)] = x;
-  }
-  if (PAY) {
-    const uint32_t *ps = P->pay[sm.buf] + sm.begin;
-    for (int i = tid; i < len; i += kThreads) sp[i] = ps[i];
+    ka[pidx(i)] = x;
+    if (IDX) ia[pidx(i)] = xi;
   }
   __syncthreads();
-  SortItem<U, PAY> v[E];
+  // every warp sorts its 32 rows
+  if (tid < rows) {
+    K v[kVT];
+    uint32_t vi[kVT];
 #pragma unroll
-  for (int r = 0; r < E; ++r) {
-    v[r].k = xk[tid * ROW + r];
-    v[r].i = (uint32_t)(tid * E + r);
+    for (int r = 0; r < kVT; ++r) {
+      v[r] = ka[tid * (kVT + 1) + r];
+      vi[r] = IDX ? ia[tid * (kVT + 1) + r] : 0u;
+    }
+    warp_sort<K, IDX>(v, vi);
+#pragma unroll
+    for (int r = 0; r < kVT; ++r) {
+      ka[tid * (kVT + 1) + r] = v[r];
+      if (IDX) ia[tid * (kVT + 1) + r] = vi[r];
+    }
   }
-  block_bitonic<U, PAY, E>(v, xk, xi);
-  __syncthreads();
+  // merge rounds
+  for (int R = 32 * kVT; R < len; R <<= 1) {
+    __syncthreads();
+    if (tid * kVT < len) {
+      K out[kVT];
+      uint32_t oi[kVT];
+      const int cnt = merge_thread<K, IDX>(ka, ia, tid * kVT, R, len, out, oi);
 #pragma unroll
-  for (int r = 0; r < E; ++r) xk[tid * ROW + r] = v[r].k;
-  if (PAY) {
-    __syncthreads();  // xi (the exchange scratch) becomes the index row buffer
-#pragma unroll
-    for (int r = 0; r < E; ++r) xi[tid * ROW + r] = v[r].i;
+      for (int r = 0; r < kVT; ++r)
+        if (r < cnt) {
+          kb[tid * (kVT + 1) + r] = out[r];
+          if (IDX) ib[tid * (kVT + 1) + r] = oi[r];
+        }
+    }
+    K *tk = ka; ka = kb; kb = tk;
+    uint32_t *ti = ia; ia = ib; ib = ti;
   }
   __syncthreads();
   U *dst = reinterpret_cast<U *>(P->keys[0]) + sm.begin;
   const bool dst_raw = P->raw[0] != 0;
-  uint32_t *pd = PAY ? P->pay[0] + sm.begin : nullptr;
+  if (PAY) {
+    // payloads gathered by local index straight from the source (an L1/L2
+    // resident window) into the free merge buffer, all before any is written
+    // (the source may be buffer 0 itself)
+    const uint32_t *ps = P->pay[sm.buf] + sm.begin;
+    uint32_t *stage = reinterpret_cast<uint32_t *>(kb);
+    for (int i = tid; i < len; i += kThreads)
+      stage[i] = ps[M::kPack ? (uint32_t)ka[pidx(i)] : ia[pidx(i)]];
+    __syncthreads();
+    uint32_t *pd = P->pay[0] + sm.begin;
+    for (int i = tid; i < len; i += kThreads) pd[i] = stage[i];
+  }
   for (int i = tid; i < len; i += kThreads) {
-    const U x = xk[(i / E) * ROW + (i % E)];
-    dst[i] = dst_raw ? C::dec(x) : x;
-    if (PAY) pd[i] = sp[xi[(i / E) * ROW + (i % E)]];
+    const K x = ka[pidx(i)];
+    const U k = M::kPack ? (U)(x >> 32) : (U)x;
+    dst[i] = dst_raw ? C::dec(k) : k;
   }
 }
 
 template <class C, bool PAY>
-__global__ void __launch_bounds__(kThreads) small_sort_kernel(const Params *__restrict__ P) {
+__global__ void __launch_bounds__(kThreads, PAY ? 2 : 3) small_sort_kernel(const Params *__restrict__ P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
   Ctl *ctl = P->ctl;
@@ -230,13 +428,8 @@ __global__ void __launch_bounds__(kThreads) small_sort_kernel(const Params *__re
     __syncthreads();
     if (t >= count) break;
     const SmallSeg sm = P->smalls[t];
-    const int len = sm.len;
-    if (len <= kThreads) small_sort_one<C, PAY, 1>(P, sm, smem_raw);
-    else if (len <= 2 * kThreads) small_sort_one<C, PAY, 2>(P, sm, smem_raw);
-    else if (len <= 4 * kThreads) small_sort_one<C, PAY, 4>(P, sm, smem_raw);
-    else if (len <= 8 * kThreads) small_sort_one<C, PAY, 8>(P, sm, smem_raw);
-    else small_sort_one<C, PAY, 16>(P, sm, smem_raw);
-    elems += (uint64_t)len;
+    small_sort_one<C, PAY>(P, sm, smem_raw);
+    elems += (uint64_t)sm.len;
     __syncthreads();
   }
   if (threadIdx.x == 0 && elems) {
