@@ -9,8 +9,8 @@
 // with its pivot sampled now (select_pivot's role, pivot.py:205-248).
 //   few, large segments   one CTA per segment, 1023-key samples sorted by a
 //                         register bitonic network across the CTA
-//   many, small segments  one warp per segment, <= 255-key samples sorted in
-//                         the warp's registers; the queue slots of all of a
+//   many, small segments  one warp per (segment, child), <= 127-key samples
+//                         sorted in the warp's registers; the queue slots of all of a
 //                         CTA's segments are claimed with one atomic per
 //                         queue per round (the queues are single hot words)
 #pragma once
@@ -23,9 +23,9 @@ enum SchedStat {
   ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_COUNT
 };
 
-constexpr int kWarpSampleMax = 255;   // warp-mode sample cap (8 per lane)
+constexpr int kWarpSampleMax = 127;   // warp-mode sample cap (4 per lane)
 // Segments of at least this many keys (on average) are scheduled by a whole
-// CTA each; below it one warp per segment.
+// CTA each; below it one warp per child.
 constexpr long long kCtaScheduleMin = 1ll << 17;
 
 __device__ __forceinline__ void append_small(const Params *P, long long begin, long long len,
@@ -112,20 +112,25 @@ __device__ __forceinline__ void load_samples(const typename C::U *data, bool enc
   long long shift = 0;
   const double step = (double)span / (double)(S - 1);
   if (mitigation) shift = (long long)floor((dran - 1.0) * step * 0.5);
+  // positions first (clamped into the segment so every load is valid), then
+  // all Q loads back to back so their latencies overlap
+  const U *ptr[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
-    const int i = owner * Q + q;
-    v[q] = KeyMax<U>::v;
-    if (i < S) {
-      long long pos = (i == S - 1) ? begin + span : begin + (long long)((double)i * step);
-      if (i != 0 && i != midi && i != S - 1) {
-        pos += shift;
-        pos = pos < begin ? begin : (pos > begin + span ? begin + span : pos);
-      }
-      const U x = ldcg(data + pos);
-      v[q] = encoded_src ? x : C::enc(x);
+    const int i = min(owner * Q + q, S - 1);
+    long long pos = (i == S - 1) ? begin + span : begin + (long long)((double)i * step);
+    if (i != 0 && i != midi && i != S - 1) {
+      pos += shift;
+      pos = pos < begin ? begin : (pos > begin + span ? begin + span : pos);
     }
+    ptr[q] = data + pos;
   }
+  U x[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) x[q] = ldcg(ptr[q]);
+#pragma unroll
+  for (int q = 0; q < Q; ++q)
+    v[q] = owner * Q + q < S ? (encoded_src ? x[q] : C::enc(x[q])) : KeyMax<U>::v;
 }
 
 // order flag of the samples in position order (+1 nondecreasing, -1
@@ -166,6 +171,9 @@ __device__ __forceinline__ typename C::U warp_pivot_q(const typename C::U *data,
                                                       long long begin, long long len, int S,
                                                       double dran, int mitigation, int *flag) {
   typedef typename C::U U;
+  // reconverge first: after lane-0-only bookkeeping the warp may still run
+  // split, and the network's shuffles would take the divergent slow path
+  __syncwarp();
   U v[Q];
   load_samples<C, Q>(data, enc_src, begin, len, S, dran, mitigation, threadIdx.x & 31, v);
   *flag = warp_order_flag<U, Q>(v, S);
@@ -241,7 +249,8 @@ __device__ typename C::U cta_select_pivot_fast(const typename C::U *data, bool e
 
 template <class C, bool PAY, bool CTA>
 __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u64 *st,
-                             long long *lt_out, long long *gt_out, uint32_t *requeue) {
+                             long long *lt_out, long long *gt_out, uint32_t *requeue,
+                             bool bookkeep = true) {
   typedef typename C::U U;
   const int r = CTA ? (int)threadIdx.x : (int)(threadIdx.x & 31);
   const int gsize = CTA ? kThreads : 32;
@@ -251,6 +260,7 @@ __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u
   const int kb = (int)sizeof(U);
   *requeue = 0;
   if (sg.kind != KIND_PARTITION) {
+    if (!bookkeep) return false;
     if (sg.fail == 0) {
       const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
       if (leader) {
@@ -275,6 +285,9 @@ __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u
   const long long lt = (long long)((inc >> 31) & 0x7fffffffull);
   const long long gt = (long long)(inc & 0x7fffffffull);
   const long long eq = len - lt - gt;
+  *lt_out = lt;
+  *gt_out = gt;
+  if (!bookkeep) return !P->single_stage;
   if (leader) {
     atomicAdd(&st[ST_STAGES], 1ull);
     atomicAdd(&st[ST_PARTITIONED], (u64)len);
@@ -338,8 +351,12 @@ struct RoundShared {
   uint32_t lv_slot0, lv_tile0, run_slot0, run_chunk0, sm_slot0;
 };
 
+// Warp mode: one task per warp, task = (segment, child); the child-0 warp
+// also does the segment's bookkeeping (statistics, == p run, verified runs,
+// re-queued verifications), so the two pivot samplings of a segment run on
+// two warps side by side.
 template <class C, bool PAY>
-__device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t sid, bool have,
+__device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t task, bool have,
                                     u64 *st, RoundShared &rs) {
   typedef typename C::U U;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -350,12 +367,15 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
   }
   __syncwarp();
   if (have) {
+    const uint32_t sid = task >> 1;
+    const int c = (int)(task & 1u);
     const Seg sg = P->segs[cur][sid];
     long long lt = 0, gt = 0;
     uint32_t requeue = 0;
-    const bool kids = segment_head<C, PAY, false>(P, nxt, sg, cur, st, &lt, &gt, &requeue);
+    const bool kids =
+        segment_head<C, PAY, false>(P, nxt, sg, cur, st, &lt, &gt, &requeue, c == 0);
     const long long len = sg.end - sg.begin;
-    if (lane == 0) {
+    if (lane == 0 && c == 0) {
       if (sg.kind != KIND_PARTITION) {
         if (requeue) {
           ReqLevel &q = rs.lv[warp][0];
@@ -379,26 +399,20 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         }
       }
     }
-    if (kids) {
+    const long long cb = c == 0 ? sg.begin : sg.end - gt;
+    const long long cl = c == 0 ? lt : gt;
+    if (kids && cl > 0) {
       const uint32_t db = sg.buf ^ 1u;
       const uint32_t depth = sg.depth + 1;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const long long cb = c == 0 ? sg.begin : sg.end - gt;
-        const long long cl = c == 0 ? lt : gt;
-        if (cl <= 0) continue;
-        if (cl <= P->small_t) {
-          if (lane == 0) {
-            ReqSmall &q = rs.sm[warp][c];
-            q.begin = cb; q.len = cl; q.buf = db; q.valid = 1;
-            atomicMax(&st[ST_DEPTH], (u64)depth);
-          }
-          continue;
+      if (cl <= P->small_t) {
+        if (lane == 0) {
+          ReqSmall &q = rs.sm[warp][0];
+          q.begin = cb; q.len = cl; q.buf = db; q.valid = 1;
+          atomicMax(&st[ST_DEPTH], (u64)depth);
         }
-        if ((int)depth > P->max_depth) {
-          if (lane == 0) atomicOr(&P->ctl->error, (uint32_t)ERR_DEPTH);
-          continue;
-        }
+      } else if ((int)depth > P->max_depth) {
+        if (lane == 0) atomicOr(&P->ctl->error, (uint32_t)ERR_DEPTH);
+      } else {
         int flag = 0;
         const U piv = warp_select_pivot<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
                                            cb, cl, P->dran, P->mitigation, &flag);
@@ -406,7 +420,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
           uint32_t kind = KIND_PARTITION;
           if (P->fast_paths)
             kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
-          ReqLevel &q = rs.lv[warp][c];
+          ReqLevel &q = rs.lv[warp][0];
           q.begin = cb; q.end = cb + cl; q.pivot = (u64)piv; q.buf = db; q.kind = kind;
           q.depth = depth; q.noverify = 0; q.ntiles = tiles_of<C, PAY>(cb, cb + cl); q.valid = 1;
         }
@@ -646,9 +660,10 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
       schedule_segment_cta<C, PAY>(P, cur, nxt, sid, xk, st, bcast);
   } else {
     const uint32_t per_round = gridDim.x * (kThreads / 32);
-    for (uint32_t base = blockIdx.x * (kThreads / 32); base < nseg; base += per_round) {
-      const uint32_t sid = base + (threadIdx.x >> 5);
-      schedule_round_warp<C, PAY>(P, cur, nxt, sid, sid < nseg, st, rs);
+    const uint32_t ntask = 2 * nseg;
+    for (uint32_t base = blockIdx.x * (kThreads / 32); base < ntask; base += per_round) {
+      const uint32_t task = base + (threadIdx.x >> 5);
+      schedule_round_warp<C, PAY>(P, cur, nxt, task, task < ntask, st, rs);
     }
   }
   __syncthreads();
