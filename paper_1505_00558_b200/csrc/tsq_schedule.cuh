@@ -7,7 +7,7 @@
 // (never compared again), then queue each child -- the < part and the > part
 // -- either for the on-chip sort (<= small_t keys) or for the next level
 // with its pivot sampled now (select_pivot's role, pivot.py:205-248).
-//   few, large segments   one CTA per segment, 1023-key samples sorted by a
+//   few, large segments   one CTA per (segment, child), 1023-key samples sorted by a
 //                         register bitonic network across the CTA
 //   many, small segments  one warp per (segment, child), <= 127-key samples
 //                         sorted in the warp's registers; the queue slots of all of a
@@ -25,8 +25,8 @@ enum SchedStat {
 
 constexpr int kWarpSampleMax = 127;   // warp-mode sample cap (4 per lane)
 // Segments of at least this many keys (on average) are scheduled by a whole
-// CTA each; below it one warp per child.
-constexpr long long kCtaScheduleMin = 1ll << 17;
+// CTA per child; below it one warp per child.
+constexpr long long kCtaScheduleMin = 1ll << 20;
 
 __device__ __forceinline__ void append_small(const Params *P, long long begin, long long len,
                                              uint32_t buf) {
@@ -582,17 +582,24 @@ __device__ void cta_append_run(const Params *P, uint32_t kind, long long begin, 
   __syncthreads();
 }
 
+// CTA mode: one CTA per (segment, child); the child-0 CTA also does the
+// segment's bookkeeping.
 template <class C, bool PAY>
-__device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t sid,
+__device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t task,
                                      typename C::U *xk, u64 *st, volatile uint32_t *bc) {
   typedef typename C::U U;
+  const uint32_t sid = task >> 1;
+  const int only = (int)(task & 1u);
   const Seg sg = P->segs[cur][sid];
   long long lt = 0, gt = 0;
   uint32_t requeue = 0;
-  const bool kids = segment_head<C, PAY, true>(P, nxt, sg, cur, st, &lt, &gt, &requeue);
+  const bool kids =
+      segment_head<C, PAY, true>(P, nxt, sg, cur, st, &lt, &gt, &requeue, only == 0);
   __syncthreads();
   const long long len = sg.end - sg.begin;
-  if (sg.kind != KIND_PARTITION) {
+  if (only == 1) {
+    if (!kids) return;
+  } else if (sg.kind != KIND_PARTITION) {
     if (requeue) {
       cta_append_level<C, PAY>(P, nxt, sg.begin, sg.end, sg.buf, sg.pivot, KIND_PARTITION,
                                sg.depth, 1, bc);
@@ -604,24 +611,26 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
     return;
   }
   const long long eq = len - lt - gt;
-  if (eq > 0 && !PAY) cta_append_run(P, RUN_EQ, sg.begin + lt, eq, sg.buf, sg.pivot, sg.begin, bc);
+  if (only == 0 && eq > 0 && !PAY)
+    cta_append_run(P, RUN_EQ, sg.begin + lt, eq, sg.buf, sg.pivot, sg.begin, bc);
   if (!kids) return;
   const uint32_t db = sg.buf ^ 1u;
   const uint32_t depth = sg.depth + 1;
-  for (int c = 0; c < 2; ++c) {
+  {
+    const int c = only;
     const long long cb = c == 0 ? sg.begin : sg.end - gt;
     const long long cl = c == 0 ? lt : gt;
-    if (cl <= 0) continue;
+    if (cl <= 0) return;
     if (cl <= P->small_t) {
       if (threadIdx.x == 0) {
         append_small(P, cb, cl, db);
         atomicMax(&st[ST_DEPTH], (u64)depth);
       }
-      continue;
+      return;
     }
     if ((int)depth > P->max_depth) {
       if (threadIdx.x == 0) atomicOr(&P->ctl->error, (uint32_t)ERR_DEPTH);
-      continue;
+      return;
     }
     int flag = 0;
     const U piv = cta_select_pivot_fast<C>(reinterpret_cast<const U *>(P->keys[db]),
@@ -656,8 +665,8 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
   const long long avg = nseg ? ((long long)ctl->cur_ntiles * Geo<C, PAY>::TILE) / nseg : 0;
   if (avg >= kCtaScheduleMin) {
     U *xk = reinterpret_cast<U *>(smem_raw);
-    for (uint32_t sid = blockIdx.x; sid < nseg; sid += gridDim.x)
-      schedule_segment_cta<C, PAY>(P, cur, nxt, sid, xk, st, bcast);
+    for (uint32_t task = blockIdx.x; task < 2 * nseg; task += gridDim.x)
+      schedule_segment_cta<C, PAY>(P, cur, nxt, task, xk, st, bcast);
   } else {
     const uint32_t per_round = gridDim.x * (kThreads / 32);
     const uint32_t ntask = 2 * nseg;
