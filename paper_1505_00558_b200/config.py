@@ -50,9 +50,10 @@ class GpuConfig:
                  reversed (the _sorted_handler / _reversed_handler role,
                  core.py:991-1556); results are identical either way.
     max_depth    depth guard; exceeding it raises instead of degrading.
-    small_threshold  segments of at most this many keys finish in the on-chip
-                 sorting network (lower it to drive the partition machine on
-                 tiny inputs, like the reference tests' insertion_threshold=3)
+    small_threshold  segments of at most this many keys (<= 8192) finish in the
+                 on-chip sort; 0 = 8192 for 4-byte keys, 4096 for 8-byte keys
+                 (lower it to drive the partition machine on tiny inputs, like
+                 the reference tests' insertion_threshold=3)
     host_levels  drive recursion levels from the host with a per-level trace
                  (debug / measurement); the default runs the whole recursion
                  inside one CUDA graph with a device-side loop.
@@ -68,12 +69,12 @@ class GpuConfig:
     fast_paths: bool = True
     max_depth: int = 96
     host_levels: bool = False
-    small_threshold: int = 4096
+    small_threshold: int = 0
     reproducible: bool = False
 
     def __post_init__(self):
-        if not 1 <= self.small_threshold <= 4096:
-            raise ValueError("small_threshold must be in [1, 4096]")
+        if not (self.small_threshold == 0 or 1 <= self.small_threshold <= 8192):
+            raise ValueError("small_threshold must be 0 (auto) or in [1, 8192]")
         if not 8 <= self.max_depth <= 190:
             raise ValueError("max_depth must be in [8, 190]")
 

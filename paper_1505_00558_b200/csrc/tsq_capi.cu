@@ -20,7 +20,8 @@ namespace {
 struct KernelSet {
   const void *init, *part, *sched, *small, *retire, *selp;
   int key_bytes, tile;
-  size_t part_smem, sched_smem, small_smem;
+  size_t part_smem, sched_smem, small_smem, small2_smem;
+  const void *small2;  // 512-thread on-chip sort (segments of kSmallT+1 .. kSmallMax)
 };
 
 template <int DT, bool PAY>
@@ -31,7 +32,8 @@ KernelSet make_set() {
   s.init = reinterpret_cast<const void *>(&init_kernel<C, PAY>);
   s.part = reinterpret_cast<const void *>(&partition_kernel<C, PAY>);
   s.sched = reinterpret_cast<const void *>(&schedule_kernel<C, PAY>);
-  s.small = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY>);
+  s.small = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, kThreads>);
+  s.small2 = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 2 * kThreads>);
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
   s.key_bytes = (int)sizeof(U);
@@ -43,6 +45,7 @@ KernelSet make_set() {
     typedef MergeTraits<Codec<DT>, PAY> M;
     const size_t np = (size_t)kSmallT + (kSmallT >> kLogVT);
     s.small_smem = 2 * np * sizeof(typename M::K) + (M::kIdx ? 2 * np * 4 : 0);
+    s.small2_smem = 2 * s.small_smem;
   }
   return s;
 }
@@ -89,12 +92,13 @@ u64 host_enc(int dt, u64 x) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t keys_alt, pay_alt, side_pay, segs[2], tilemap[2], lookback[2], smalls, runs, chunkmap;
+  size_t keys_alt, pay_alt, side_pay, segs[2], tilemap[2], lookback[2], smalls, bigs, runs,
+      chunkmap;
   size_t total;
-  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap;
+  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap, big_cap;
 };
 
-Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallT) {
+Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallMax) {
   Layout L;
   memset(&L, 0, sizeof(L));
   const int kb = key_bytes_of(kt);
@@ -104,6 +108,7 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallT) {
   L.tile_cap = (uint32_t)(n / tile + 2ull * L.seg_cap + 2);
   L.run_cap = 8u * L.seg_cap + 64u;
   L.small_cap = 2u * L.run_cap;
+  L.big_cap = (uint32_t)(n / (size_t)(kSmallT + 1) + 2);
   L.chunk_cap = (uint32_t)(n / kRunChunk + L.run_cap + 2);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -118,6 +123,7 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallT) {
   for (int b = 0; b < 2; ++b) L.tilemap[b] = take((size_t)L.tile_cap * 4);
   for (int b = 0; b < 2; ++b) L.lookback[b] = take((size_t)L.tile_cap * 8);
   L.smalls = take((size_t)L.small_cap * sizeof(SmallSeg));
+  L.bigs = take((size_t)L.big_cap * sizeof(SmallSeg));
   L.runs = take((size_t)L.run_cap * sizeof(Run));
   L.chunkmap = take((size_t)L.chunk_cap * 4);
   L.total = off;
@@ -175,11 +181,11 @@ int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem, int block = k
 }
 
 tsq_status prepare_small_smem(const KernelSet &ks) {
-  const void *fns[3] = {ks.part, ks.sched, ks.small};
-  const size_t sm[3] = {ks.part_smem, ks.sched_smem, ks.small_smem};
+  const void *fns[4] = {ks.part, ks.sched, ks.small, ks.small2};
+  const size_t sm[4] = {ks.part_smem, ks.sched_smem, ks.small_smem, ks.small2_smem};
   // always opt in: dynamic + static shared memory may cross 48 KB even when
   // the dynamic part alone does not
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 4; ++i)
     TSQ_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sm[i]));
   return TSQ_OK;
@@ -226,6 +232,8 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
     p->lookback[b] = reinterpret_cast<u64 *>(base + L.lookback[b]);
   }
   p->smalls = reinterpret_cast<SmallSeg *>(base + L.smalls);
+  p->bigs = reinterpret_cast<SmallSeg *>(base + L.bigs);
+  p->big_cap = L.big_cap;
   p->runs = reinterpret_cast<Run *>(base + L.runs);
   p->chunkmap = reinterpret_cast<uint32_t *>(base + L.chunkmap);
   p->seg_cap = L.seg_cap;
@@ -238,7 +246,7 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
   p->fast_paths = 1;
   p->mitigation = 1;
   p->dran = 1.0;
-  p->small_t = kSmallT;
+  p->small_t = kSmallMax;
   p->reproducible = 0;
 }
 
@@ -304,18 +312,25 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   sk.gridDim = dim3(occupancy_grid(ws, ks.small, ks.small_smem));
   sk.sharedMemBytes = (unsigned)ks.small_smem;
   TSQ_CUDA(cudaGraphAddKernelNode(&snode, g, &e2, 1, &sk));
+  cudaKernelNodeParams sk2 = lk;
+  sk2.func = const_cast<void *>(ks.small2);
+  sk2.gridDim = dim3(occupancy_grid(ws, ks.small2, ks.small2_smem, 2 * kThreads));
+  sk2.blockDim = dim3(2 * kThreads);
+  sk2.sharedMemBytes = (unsigned)ks.small2_smem;
+  cudaGraphNode_t snode2;
+  TSQ_CUDA(cudaGraphAddKernelNode(&snode2, g, &e2, 1, &sk2));
   cudaKernelNodeParams rk = lk;
   rk.func = const_cast<void *>(ks.retire);
   rk.gridDim = dim3(occupancy_grid(ws, ks.retire, 0));
   rk.sharedMemBytes = 0;
   TSQ_CUDA(cudaGraphAddKernelNode(&rnode, g, &e2, 1, &rk));
-  cudaGraphNode_t tail[2] = {snode, rnode};
-  TSQ_CUDA(cudaGraphAddEventRecordNode(&e3, g, tail, 2, ge->ev[3]));
+  cudaGraphNode_t tail[3] = {snode, snode2, rnode};
+  TSQ_CUDA(cudaGraphAddEventRecordNode(&e3, g, tail, 3, ge->ev[3]));
   TSQ_CUDA(cudaGraphInstantiate(&ge->exec, g, 0));
   return TSQ_OK;
 }
 
-tsq_status reserve_locked(tsq_workspace *ws, size_t n, int kt, int pt, int small_t = kSmallT) {
+tsq_status reserve_locked(tsq_workspace *ws, size_t n, int kt, int pt, int small_t = kSmallMax) {
   const Layout L = make_layout(n, kt, pt, small_t);
   if (L.total <= ws->block_bytes) {
     if (n > ws->cap_elems) ws->cap_elems = n;
@@ -360,7 +375,7 @@ tsq_status fill_stats(tsq_workspace *ws, size_t n, tsq_stats *st) {
   st->stages = c.stages;
   st->levels = c.levels;
   st->max_depth = c.max_depth;
-  st->small_segments = c.small_count;
+  st->small_segments = (u64)c.small_count + (u64)c.big_count;
   st->eq_runs = c.eq_runs;
   st->eq_elements = c.eq_elements;
   st->sorted_bypass = c.sorted_bypass;
@@ -508,9 +523,11 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     if (stats) stats->n = n;
     return TSQ_OK;
   }
-  int small_t = kSmallT;
+  // default cut: the 512-thread class pays for 4-byte keys; 8-byte keys fit
+  // its shared memory only one CTA per SM, so they stop at the 256 class
+  int small_t = key_bytes_of(key_t) == 4 ? kSmallMax : kSmallT;
   if (params && params->small_threshold > 0)
-    small_t = params->small_threshold < kSmallT ? params->small_threshold : kSmallT;
+    small_t = params->small_threshold < kSmallMax ? params->small_threshold : kSmallMax;
   // allocation precedes any mutation (core.py:1599, TempAllocationError)
   st = reserve_locked(ws, n, key_t, payload_t, small_t);
   if (st != TSQ_OK) return st;
@@ -612,6 +629,9 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   }
   TSQ_CUDA(cudaLaunchKernel(ks.small, dim3(occupancy_grid(ws, ks.small, ks.small_smem)),
                             dim3(kThreads), largs, ks.small_smem, s));
+  TSQ_CUDA(cudaLaunchKernel(ks.small2,
+                            dim3(occupancy_grid(ws, ks.small2, ks.small2_smem, 2 * kThreads)),
+                            dim3(2 * kThreads), largs, ks.small2_smem, s));
   TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
                             largs, 0, s));
   TSQ_CUDA(cudaEventRecord(t1, s));

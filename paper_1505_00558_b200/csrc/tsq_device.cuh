@@ -20,7 +20,8 @@ namespace tsq {
 typedef unsigned long long u64;
 
 constexpr int kThreads = 256;        // every kernel: 8 warps per CTA
-constexpr int kSmallT = 4096;        // segments <= this finish on chip
+constexpr int kSmallT = 4096;        // on-chip sort, 256-thread class (<= this)
+constexpr int kSmallMax = 8192;      // on-chip sort, 512-thread class; default cut
 constexpr int kMaxSample = 1023;     // pivot sample size cap (2^10 - 1)
 constexpr int kRunChunk = 8192;      // elements per retire work item
 constexpr int kMaxLevels = 200;      // hard stop for the level loop
@@ -50,7 +51,7 @@ struct Seg {
   uint32_t fail;
 };
 
-// A segment of <= kSmallT elements waiting for the on-chip sort.
+// A segment of <= kSmallMax elements waiting for the on-chip sort.
 struct SmallSeg {
   long long begin;
   int len;
@@ -75,7 +76,8 @@ struct Ctl {
   uint32_t level, tile_ticket;
   uint32_t ctas_done, small_count;
   uint32_t small_ticket, run_ticket;
-  uint32_t error, pad0;
+  uint32_t error, big_count;  // big_count: segments queued for the 512-thread sort
+  uint32_t big_ticket, pad0;
   u64 stages, max_depth, levels, eq_runs, eq_elements;
   u64 sorted_bypass, reversed_bypass, verify_fallbacks;
   u64 partitioned_elements, small_elements;
@@ -102,10 +104,11 @@ struct Params {
   Seg *segs[2];
   uint32_t *tilemap[2];
   u64 *lookback[2];
-  SmallSeg *smalls;
+  SmallSeg *smalls;       // on-chip sort queue, <= kSmallT keys
+  SmallSeg *bigs;         // on-chip sort queue, (kSmallT, kSmallMax] keys
   Run *runs;
   uint32_t *chunkmap;
-  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap, pad1;
+  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap, big_cap;
   Ctl *ctl;
   cudaGraphConditionalHandle cond;
 };

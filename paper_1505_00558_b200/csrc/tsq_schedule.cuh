@@ -31,11 +31,12 @@ constexpr long long kCtaScheduleMin = 1ll << 20;
 __device__ __forceinline__ void append_small(const Params *P, long long begin, long long len,
                                              uint32_t buf) {
   Ctl *ctl = P->ctl;
-  const uint32_t slot = atomicAdd(&ctl->small_count, 1u);
-  if (slot < P->small_cap) {
+  const bool big = len > kSmallT;  // the 512-thread class
+  const uint32_t slot = atomicAdd(big ? &ctl->big_count : &ctl->small_count, 1u);
+  if (slot < (big ? P->big_cap : P->small_cap)) {
     SmallSeg s;
     s.begin = begin; s.len = (int)len; s.buf = (int)buf;
-    P->smalls[slot] = s;
+    (big ? P->bigs : P->smalls)[slot] = s;
   } else {
     atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
   }
@@ -348,7 +349,7 @@ struct RoundShared {
   ReqLevel lv[kThreads / 32][2];
   ReqRun run[kThreads / 32];
   ReqSmall sm[kThreads / 32][2];
-  uint32_t lv_slot0, lv_tile0, run_slot0, run_chunk0, sm_slot0;
+  uint32_t lv_slot0, lv_tile0, run_slot0, run_chunk0, sm_slot0, bg_slot0;
 };
 
 // Warp mode: one task per warp, task = (segment, child); the child-0 warp
@@ -430,11 +431,11 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
   __syncthreads();
   // one claim per queue for the whole round
   if (threadIdx.x == 0) {
-    uint32_t nl = 0, nt = 0, nr = 0, nc = 0, ns = 0;
+    uint32_t nl = 0, nt = 0, nr = 0, nc = 0, ns = 0, nb = 0;
     for (int w = 0; w < kThreads / 32; ++w) {
       for (int c = 0; c < 2; ++c) {
         if (rs.lv[w][c].valid) { ++nl; nt += rs.lv[w][c].ntiles; }
-        if (rs.sm[w][c].valid) ++ns;
+        if (rs.sm[w][c].valid) ++(rs.sm[w][c].len > kSmallT ? nb : ns);
       }
       if (rs.run[w].valid) { ++nr; nc += rs.run[w].nchunks; }
     }
@@ -464,15 +465,22 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         rs.sm_slot0 = kDone;
       }
     }
+    if (nb) {
+      rs.bg_slot0 = atomicAdd(&ctl->big_count, nb);
+      if (rs.bg_slot0 + nb > P->big_cap) {
+        atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+        rs.bg_slot0 = kDone;
+      }
+    }
   }
   __syncthreads();
   // each warp writes its records at its offsets
   uint32_t lslot = rs.lv_slot0, ltile = rs.lv_tile0, rslot = rs.run_slot0;
-  uint32_t rchunk = rs.run_chunk0, sslot = rs.sm_slot0;
+  uint32_t rchunk = rs.run_chunk0, sslot = rs.sm_slot0, bslot = rs.bg_slot0;
   for (int w = 0; w < warp; ++w) {
     for (int c = 0; c < 2; ++c) {
       if (rs.lv[w][c].valid) { ++lslot; ltile += rs.lv[w][c].ntiles; }
-      if (rs.sm[w][c].valid) ++sslot;
+      if (rs.sm[w][c].valid) ++(rs.sm[w][c].len > kSmallT ? bslot : sslot);
     }
     if (rs.run[w].valid) { ++rslot; rchunk += rs.run[w].nchunks; }
   }
@@ -496,12 +504,13 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     }
     const ReqSmall &m = rs.sm[warp][c];
     if (m.valid) {
-      if (rs.sm_slot0 != kDone && lane == 0) {
+      const bool big = m.len > kSmallT;
+      if ((big ? rs.bg_slot0 : rs.sm_slot0) != kDone && lane == 0) {
         SmallSeg s;
         s.begin = m.begin; s.len = (int)m.len; s.buf = (int)m.buf;
-        P->smalls[sslot] = s;
+        (big ? P->bigs : P->smalls)[big ? bslot : sslot] = s;
       }
-      ++sslot;
+      ++(big ? bslot : sslot);
     }
   }
   const ReqRun &q = rs.run[warp];

@@ -326,14 +326,14 @@ __device__ __forceinline__ int merge_thread(const K *S, const uint32_t *SI, int 
   return cnt;
 }
 
-template <class C, bool PAY>
+template <class C, bool PAY, int NT>
 __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &sm,
                                                unsigned char *smem) {
   typedef typename C::U U;
   typedef MergeTraits<C, PAY> M;
   typedef typename M::K K;
   constexpr bool IDX = M::kIdx;
-  constexpr int NP = kSmallT + (kSmallT >> kLogVT);  // padded capacity
+  constexpr int NP = NT * kVT + NT;  // padded capacity (rows of kVT + 1)
   // smem: buffers A, B [NP] of K | (records, 64-bit keys) index A, B [NP]
   K *ka = reinterpret_cast<K *>(smem), *kb = ka + NP;  // current / other buffer
   uint32_t *ia = reinterpret_cast<uint32_t *>(kb + NP), *ib = ia + (IDX ? NP : 0);
@@ -344,7 +344,7 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
   const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
   const bool raw = P->raw[sm.buf] != 0;
   // coalesced load into padded rows (sentinels complete the last row)
-  for (int i = tid; i < rows * kVT; i += kThreads) {
+  for (int i = tid; i < rows * kVT; i += NT) {
     K x;
     uint32_t xi = 0xffffffffu;
     if (i < len) {
@@ -401,34 +401,42 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
     // (the source may be buffer 0 itself)
     const uint32_t *ps = P->pay[sm.buf] + sm.begin;
     uint32_t *stage = reinterpret_cast<uint32_t *>(kb);
-    for (int i = tid; i < len; i += kThreads)
+    for (int i = tid; i < len; i += NT)
       stage[i] = ps[M::kPack ? (uint32_t)ka[pidx(i)] : ia[pidx(i)]];
     __syncthreads();
     uint32_t *pd = P->pay[0] + sm.begin;
-    for (int i = tid; i < len; i += kThreads) pd[i] = stage[i];
+    for (int i = tid; i < len; i += NT) pd[i] = stage[i];
   }
-  for (int i = tid; i < len; i += kThreads) {
+  for (int i = tid; i < len; i += NT) {
     const K x = ka[pidx(i)];
     const U k = M::kPack ? (U)(x >> 32) : (U)x;
     dst[i] = dst_raw ? C::dec(k) : k;
   }
 }
 
-template <class C, bool PAY>
-__global__ void __launch_bounds__(kThreads, PAY ? 2 : 3) small_sort_kernel(const Params *__restrict__ P) {
+// One CTA per queued segment (tickets).  NT = 256: the queue of segments of
+// <= kSmallT keys; NT = 512: the queue of kSmallT+1 .. kSmallMax keys.
+template <class C, bool PAY, int NT>
+__global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : 1)
+    small_sort_kernel(const Params *__restrict__ P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
   Ctl *ctl = P->ctl;
-  const uint32_t count = ctl->small_count < P->small_cap ? ctl->small_count : P->small_cap;
+  const bool big = NT != kThreads;
+  const uint32_t n_q = big ? ctl->big_count : ctl->small_count;
+  const uint32_t cap = big ? P->big_cap : P->small_cap;
+  const uint32_t count = n_q < cap ? n_q : cap;
+  const SmallSeg *q = big ? P->bigs : P->smalls;
+  uint32_t *ticket = big ? &ctl->big_ticket : &ctl->small_ticket;
   uint64_t elems = 0;
   for (;;) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&ctl->small_ticket, 1u);
+    if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t t = s_ticket;
     __syncthreads();
     if (t >= count) break;
-    const SmallSeg sm = P->smalls[t];
-    small_sort_one<C, PAY>(P, sm, smem_raw);
+    const SmallSeg sm = q[t];
+    small_sort_one<C, PAY, NT>(P, sm, smem_raw);
     elems += (uint64_t)sm.len;
     __syncthreads();
   }

@@ -53,7 +53,7 @@ def sorter(cuda_ok, request):
     return T.Sorter(seed=1, gpu=T.GpuConfig(reproducible=request.param))
 
 
-@pytest.mark.parametrize("n", [2, 3, 17, 100, 4095, 4096, 4097, 8193, 65536, 100003, 1 << 20])
+@pytest.mark.parametrize("n", [2, 3, 17, 100, 4095, 4096, 4097, 8192, 8193, 65536, 100003, 1 << 20])
 def test_int32_sizes_vs_oracle(sorter, n):
     rng = np.random.default_rng(n)
     x = _random(np.int32, n, rng)
@@ -96,7 +96,7 @@ def test_families_vs_reference_hashes(sorter, rec):
         assert_records_consistent(keys, ko, po, np.sort(keys))
 
 
-@pytest.mark.parametrize("thr", [1, 3, 16, 4096])
+@pytest.mark.parametrize("thr", [1, 3, 16, 4096, 8192])
 def test_kat_and_exhaustive_small(cuda_ok, thr):
     """[5,3,5,1,5] KAT, exhaustive 3^8 multisets and a slice of 8!
     permutations (tests/test_core.py:28-57); small_threshold=3 drives the
