@@ -343,20 +343,28 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
   const int rows = ((len + 32 * kVT - 1) / (32 * kVT)) * 32;
   const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
   const bool raw = P->raw[sm.buf] != 0;
-  // coalesced load into padded rows (sentinels complete the last row)
-  for (int i = tid; i < rows * kVT; i += NT) {
-    K x;
-    uint32_t xi = 0xffffffffu;
-    if (i < len) {
-      U k = src[i];
-      if (raw) k = C::enc(k);
-      xi = (uint32_t)i;
-      x = M::kPack ? (K)(((u64)k << 32) | (u64)i) : (K)k;
-    } else {
-      x = ~K(0);
+  // coalesced load into padded rows (sentinels complete the last rows): all
+  // of a thread's loads issued before any is used, so their latencies overlap
+  U raw_k[kVT];
+#pragma unroll
+  for (int q = 0; q < kVT; ++q) {
+    const int i = tid + q * NT;
+    raw_k[q] = i < len ? src[i] : U(0);
+  }
+#pragma unroll
+  for (int q = 0; q < kVT; ++q) {
+    const int i = tid + q * NT;
+    if (i < rows * kVT) {
+      K x;
+      if (i < len) {
+        const U k = raw ? C::enc(raw_k[q]) : raw_k[q];
+        x = M::kPack ? (K)(((u64)k << 32) | (u64)i) : (K)k;
+      } else {
+        x = ~K(0);
+      }
+      ka[pidx(i)] = x;
+      if (IDX) ia[pidx(i)] = i < len ? (uint32_t)i : 0xffffffffu;
     }
-    ka[pidx(i)] = x;
-    if (IDX) ia[pidx(i)] = xi;
   }
   __syncthreads();
   // every warp sorts its 32 rows
@@ -417,7 +425,7 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
 // One CTA per queued segment (tickets).  NT = 256: the queue of segments of
 // <= kSmallT keys; NT = 512: the queue of kSmallT+1 .. kSmallMax keys.
 template <class C, bool PAY, int NT>
-__global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : 1)
+__global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : (PAY ? 1 : 2))
     small_sort_kernel(const Params *__restrict__ P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
