@@ -137,7 +137,29 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       // verification: every pair (i, i+1) of the segment's keys in this tile,
       // the last one against the first key of the next tile
       bool bad = false;
-      if (!m.skip) {
+      if (!m.skip && rlo == 0 && rhi == G::TILE) {
+        // whole tile: 16-byte vectors, each checked against its successor
+        const bool asc = m.kind == KIND_VERIFY_ASC;
+        constexpr int VN = G::VN;
+        constexpr int NV = G::TILE / VN;  // vectors per tile
+        const U *gk = reinterpret_cast<const U *>(P->keys[m.buf]);
+#pragma unroll 4
+        for (int v = cw * (NV / kCounterWarps) + lane; v < (cw + 1) * (NV / kCounterWarps);
+             v += 32) {
+          U k[VN + 1];
+          unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + v * VN), k);
+          bool have = true;
+          if (v + 1 < NV) k[VN] = sk[(v + 1) * VN];
+          else if (m.has_next) k[VN] = gk[m.hi];
+          else { have = false; k[VN] = k[VN - 1]; }
+#pragma unroll
+          for (int q = 0; q <= VN; ++q)
+            if (raw) k[q] = C::enc(k[q]);
+#pragma unroll
+          for (int q = 0; q < VN; ++q)
+            if (q + 1 < VN || have) bad |= asc ? (k[q] > k[q + 1]) : (k[q] < k[q + 1]);
+        }
+      } else if (!m.skip) {
         const bool asc = m.kind == KIND_VERIFY_ASC;
         for (int i = rlo + cw * 32 + lane; i < rhi; i += 32 * kCounterWarps) {
           U a = sk[i], b = a;

@@ -147,6 +147,8 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
 
 
 // Retire finished runs into buffer 0, chunk by chunk.
+constexpr int kRB = 8;  // loads in flight per thread
+
 template <class C, bool PAY>
 __global__ void __launch_bounds__(kThreads) retire_kernel(const Params *__restrict__ P) {
   typedef typename C::U U;
@@ -165,6 +167,8 @@ __global__ void __launch_bounds__(kThreads) retire_kernel(const Params *__restri
     const Run r = P->runs[P->chunkmap[c]];
     const long long cc = (long long)(c - r.chunk_base);
     const long long lo = cc * kRunChunk;
+    // every loop below issues kRB loads per thread before its stores, so
+    // the loads overlap (the buffers may alias: no reordering otherwise)
     if (r.kind == RUN_EQ) {
       const long long hi = (lo + kRunChunk) < r.len ? (lo + kRunChunk) : r.len;
       const U v = raw0 ? C::dec((U)r.pivot) : (U)r.pivot;
@@ -172,41 +176,61 @@ __global__ void __launch_bounds__(kThreads) retire_kernel(const Params *__restri
         k0[r.begin + i] = v;
         if (PAY) p0[r.begin + i] = P->side_pay[r.src + i];
       }
-    } else if (r.kind == RUN_SORTED) {
+    } else if (r.kind == RUN_SORTED || r.buf != 0) {
+      // copy (sorted run) or reversed copy from the workspace into buffer 0
+      const bool rev = r.kind == RUN_REVERSED;
       const long long hi = (lo + kRunChunk) < r.len ? (lo + kRunChunk) : r.len;
       const U *kb = reinterpret_cast<const U *>(P->keys[r.buf]);
+      const uint32_t *pb = PAY ? P->pay[r.buf] : nullptr;
       const bool rawb = P->raw[r.buf] != 0;
-      for (long long i = lo + threadIdx.x; i < hi; i += kThreads) {
-        U v = kb[r.begin + i];
-        if (rawb != raw0) v = rawb ? C::enc(v) : C::dec(v);
-        k0[r.begin + i] = v;
-        if (PAY) p0[r.begin + i] = P->pay[r.buf][r.begin + i];
-      }
-    } else {  // RUN_REVERSED
-      if (r.buf == 0) {
-        const long long half = r.len >> 1;
-        const long long hi = (lo + kRunChunk) < half ? (lo + kRunChunk) : half;
-        for (long long i = lo + threadIdx.x; i < hi; i += kThreads) {
-          const long long a = r.begin + i, b = r.begin + r.len - 1 - i;
-          const U x = k0[a], y = k0[b];
-          k0[a] = y;
-          k0[b] = x;
-          if (PAY) {
-            const uint32_t px = p0[a], py = p0[b];
-            p0[a] = py;
-            p0[b] = px;
+      for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += (long long)kThreads * kRB) {
+        U v[kRB];
+        uint32_t pv[kRB];
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) {
+          const long long i = i0 + (long long)q * kThreads;
+          if (i < hi) {
+            const long long s = rev ? r.begin + r.len - 1 - i : r.begin + i;
+            v[q] = kb[s];
+            if (PAY) pv[q] = pb[s];
           }
         }
-      } else {
-        const long long hi = (lo + kRunChunk) < r.len ? (lo + kRunChunk) : r.len;
-        const U *kb = reinterpret_cast<const U *>(P->keys[r.buf]);
-        const bool rawb = P->raw[r.buf] != 0;
-        for (long long i = lo + threadIdx.x; i < hi; i += kThreads) {
-          const long long s = r.begin + r.len - 1 - i;
-          U v = kb[s];
-          if (rawb != raw0) v = rawb ? C::enc(v) : C::dec(v);
-          k0[r.begin + i] = v;
-          if (PAY) p0[r.begin + i] = P->pay[r.buf][s];
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) {
+          const long long i = i0 + (long long)q * kThreads;
+          if (i < hi) {
+            U x = v[q];
+            if (rawb != raw0) x = rawb ? C::enc(x) : C::dec(x);
+            k0[r.begin + i] = x;
+            if (PAY) p0[r.begin + i] = pv[q];
+          }
+        }
+      }
+    } else {  // RUN_REVERSED in buffer 0: swap the two halves' mirror pairs
+      const long long half = r.len >> 1;
+      const long long hi = (lo + kRunChunk) < half ? (lo + kRunChunk) : half;
+      for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += (long long)kThreads * kRB) {
+        U x[kRB], y[kRB];
+        uint32_t px[kRB], py[kRB];
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) {
+          const long long i = i0 + (long long)q * kThreads;
+          if (i < hi) {
+            const long long a = r.begin + i, b = r.begin + r.len - 1 - i;
+            x[q] = k0[a];
+            y[q] = k0[b];
+            if (PAY) { px[q] = p0[a]; py[q] = p0[b]; }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) {
+          const long long i = i0 + (long long)q * kThreads;
+          if (i < hi) {
+            const long long a = r.begin + i, b = r.begin + r.len - 1 - i;
+            k0[a] = y[q];
+            k0[b] = x[q];
+            if (PAY) { p0[a] = py[q]; p0[b] = px[q]; }
+          }
         }
       }
     }
