@@ -11,7 +11,7 @@ raises if the library or the device is missing (no CPU fallback).
 
 from .config import DEFAULT_CONFIG, DEFAULT_GPU_CONFIG, GpuConfig, SortConfig
 from .core import (DepthExceededError, DeviceTempStore, Records, Sorter,
-                   TempAllocationError, free_temp_storage, key_cmp, sort,
+                   TempAllocationError, free_temp_storage, key_cmp, sort, sort_many,
                    sort_with_stats)
 from .pivot import MitigationRng, rng_next
 from .stats import SortStats
@@ -39,5 +39,5 @@ __all__ = [
     "DEFAULT_CONFIG", "DEFAULT_GPU_CONFIG", "DepthExceededError", "DeviceTempStore",
     "GpuConfig", "MitigationRng", "REGISTRY", "Records", "SortConfig", "SortStats", "Sorter",
     "TempAllocationError", "free_temp_storage", "get_algorithm", "key_cmp", "rng_next",
-    "sort", "sort_with_stats",
+    "sort", "sort_many", "sort_with_stats",
 ]

@@ -39,8 +39,8 @@ from .pivot import MitigationRng
 from .stats import SortStats
 
 __all__ = ["TempAllocationError", "DepthExceededError", "Records", "key_cmp",
-           "DeviceTempStore", "Sorter", "sort", "sort_with_stats", "free_temp_storage",
-           "default_sorter"]
+           "DeviceTempStore", "Sorter", "sort", "sort_with_stats", "sort_many",
+           "free_temp_storage", "default_sorter"]
 
 
 class TempAllocationError(MemoryError):
@@ -203,6 +203,84 @@ class Sorter:
             return self._sort(ar, cmp, element_size)
         finally:
             self._active = False
+
+    def sort_many(self, arrays, cmp=None) -> list:
+        """Sort a sequence of host arrays, each in place, as a pipeline.
+
+        Extension beyond the reference API for host-resident batches: the
+        host->device copy of array i+1 and the device->host copy of array i-1
+        run on their own streams (the copy engines work both directions at
+        once) while array i sorts, so a batch costs about max(H2D, D2H, sort)
+        per array instead of their sum.  Every array must be a contiguous 1-D
+        CPU tensor (pinned memory for real overlap) or numpy array of one
+        native key dtype; device tensors, lists and records go through sort().
+        Returns one SortStats per array.
+        """
+        torch = _torch()
+        if cmp is not None:
+            raise TypeError("sort_many sorts native keys only (cmp=None)")
+        items = []
+        for a in arrays:
+            t = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
+            if not isinstance(t, torch.Tensor) or t.is_cuda or t.dim() != 1 \
+                    or not t.is_contiguous():
+                raise TypeError("sort_many takes contiguous 1-D host arrays")
+            items.append(t)
+        if not items:
+            return []
+        dtype = items[0].dtype
+        if any(t.dtype != dtype for t in items):
+            raise TypeError("sort_many needs one key dtype across the batch")
+        if dtype not in _dtype_codes():
+            raise TypeError(f"unsupported key dtype {dtype}")
+        dev = self._device()
+        nmax = max(t.numel() for t in items)
+        # three device buffers: array i sorts in one while array i+1 lands in
+        # the next and array i-1 drains from the third
+        NB = 3
+        bufs = []
+        for k in range(NB):
+            b = self._staging.get(f"pipe{k}")
+            if b is None or b.dtype != dtype or b.numel() < nmax:
+                try:
+                    b = torch.empty(nmax, dtype=dtype, device=f"cuda:{dev}")
+                except torch.OutOfMemoryError as exc:
+                    raise TempAllocationError("cannot allocate the pipeline buffers") from exc
+                self._staging[f"pipe{k}"] = b
+            bufs.append(b)
+        compute = torch.cuda.current_stream(dev)
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event() for _ in range(NB)]
+        ev_out = [torch.cuda.Event() for _ in range(NB)]
+        ev_sorted = torch.cuda.Event()
+        used = [False] * NB
+
+        def h2d(i):
+            k, t = i % NB, items[i]
+            if used[k]:
+                s_in.wait_event(ev_out[k])  # the D2H of array i-NB has drained it
+            with torch.cuda.stream(s_in):
+                bufs[k][:t.numel()].copy_(t, non_blocking=True)
+                ev_in[k].record(s_in)
+            used[k] = True
+
+        out = []
+        h2d(0)
+        for i, t in enumerate(items):
+            if i + 1 < len(items):
+                h2d(i + 1)
+            k = i % NB
+            compute.wait_event(ev_in[k])
+            st = self.sort_with_stats(bufs[k][:t.numel()])
+            st.gpu["h2d_bytes"] = st.gpu["d2h_bytes"] = t.numel() * t.element_size()
+            out.append(st)
+            ev_sorted.record(compute)
+            s_out.wait_event(ev_sorted)
+            with torch.cuda.stream(s_out):
+                t.copy_(bufs[k][:t.numel()], non_blocking=True)
+                ev_out[k].record(s_out)
+        s_out.synchronize()
+        return out
 
     def free_temp_storage(self) -> None:
         """Release the retained workspace; the next sort reallocates."""
@@ -423,6 +501,11 @@ def sort(ar, cmp=None, config: SortConfig | None = None,
 def sort_with_stats(ar, cmp=None, config: SortConfig | None = None,
                     element_size: int | None = None) -> SortStats:
     return sort(ar, cmp, config, element_size)
+
+
+def sort_many(arrays, cmp=None) -> list:
+    """Pipelined in-place sort of host arrays with the default sorter."""
+    return default_sorter.sort_many(arrays, cmp)
 
 
 def free_temp_storage() -> None:

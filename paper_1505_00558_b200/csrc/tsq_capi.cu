@@ -150,6 +150,7 @@ struct tsq_workspace {
   uint64_t alloc_count = 0;
   Params *d_params = nullptr;
   Ctl *d_ctl = nullptr;
+  Ctl *h_ctl_dev = nullptr;  // device alias of the mapped host copy h_ctl
   Ctl *h_ctl = nullptr;
   cudaEvent_t done = nullptr;
   bool active = false;
@@ -362,8 +363,14 @@ tsq_status check_args(size_t n, int kt, int pt) {
   return TSQ_OK;
 }
 
+// The control block comes back through mapped host memory written by a tiny
+// kernel, not a memcpy: a copy would queue on the copy engine behind any
+// large device->host transfer in flight on other streams (sort_many's
+// pipeline), stalling the host for that transfer's duration.
 tsq_status read_ctl(tsq_workspace *ws, cudaStream_t s) {
-  TSQ_CUDA(cudaMemcpyAsync(ws->h_ctl, ws->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+  void *args[2] = {&ws->d_ctl, &ws->h_ctl_dev};
+  TSQ_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(&publish_ctl_kernel), dim3(1),
+                            dim3(32), args, 0, s));
   TSQ_CUDA(cudaStreamSynchronize(s));
   return TSQ_OK;
 }
@@ -439,7 +446,8 @@ tsq_status tsq_workspace_create(tsq_workspace **out, int device) {
   cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (cudaMalloc(&ws->d_params, sizeof(Params)) != cudaSuccess ||
       cudaMalloc(&ws->d_ctl, sizeof(Ctl)) != cudaSuccess ||
-      cudaMallocHost(&ws->h_ctl, sizeof(Ctl)) != cudaSuccess) {
+      cudaHostAlloc(&ws->h_ctl, sizeof(Ctl), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&ws->h_ctl_dev, ws->h_ctl, 0) != cudaSuccess) {
     cudaGetLastError();
     tsq_workspace_destroy(ws);
     return TSQ_ERR_ALLOC;

@@ -237,6 +237,14 @@ __global__ void __launch_bounds__(kThreads) retire_kernel(const Params *__restri
   }
 }
 
+// Copy the control block to mapped host memory (read_ctl).
+__global__ void publish_ctl_kernel(const Ctl *ctl, Ctl *host) {
+  const u64 *s = reinterpret_cast<const u64 *>(ctl);
+  volatile u64 *d = reinterpret_cast<volatile u64 *>(host);
+  for (unsigned i = threadIdx.x; i < sizeof(Ctl) / sizeof(u64); i += blockDim.x) d[i] = s[i];
+  __threadfence_system();
+}
+
 // Pivot-sampling entry for tsq_select_pivot: one CTA over keys[0..n) of
 // buffer 0; writes (pivot, flag) into the control block.
 template <class C>

@@ -337,3 +337,24 @@ def test_depth_guard_raises(cuda_ok):
     s = T.Sorter(seed=1, gpu=T.GpuConfig(max_depth=8))
     with pytest.raises(T.DepthExceededError):
         s.sort(_dev(x))
+
+
+def test_sort_many_pipeline(cuda_ok):
+    """Batch of host arrays sorted in place through the copy/sort pipeline."""
+    rng = np.random.default_rng(11)
+    sizes = [1 << 20, 3, 100003, 1 << 18, 0, 1]
+    arrays = [rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32) for n in sizes]
+    hosts = [torch.from_numpy(a.copy()).pin_memory() for a in arrays]
+    stats = T.sort_many(hosts)
+    assert len(stats) == len(hosts)
+    for h, a in zip(hosts, arrays):
+        assert np.array_equal(h.numpy(), np.sort(a))
+    # numpy (pageable) arrays too, results in place
+    nps = [a.copy() for a in arrays[:3]]
+    T.Sorter(seed=2).sort_many(nps)
+    for h, a in zip(nps, arrays):
+        assert np.array_equal(h, np.sort(a))
+    with pytest.raises(TypeError):
+        T.sort_many([np.zeros(4, np.int32), np.zeros(4, np.int64)])
+    with pytest.raises(TypeError):
+        T.sort_many([torch.zeros(4, dtype=torch.int32, device="cuda")])
