@@ -2,20 +2,20 @@
 // entry.  Included by tsq_partition.cuh after the producer and look-back
 // warps.
 //
-//   counter warps (2)  take alternate stages as soon as they land and count
-//                      the <, ==, > keys each consumer warp owns; the tile's
-//                      aggregate is published for the look-back right away --
-//                      counting never waits on anything but the data, so a
-//                      landed tile never holds up a later tile's look-back.
+//   counter warps (4)  all take every tile as soon as it lands, each
+//                      counting two consumer warps' keys: per consumer
+//                      thread the (<, >, valid) counts and their exclusive
+//                      lane prefix; the last one to finish combines the tile
+//                      aggregate and hands the stage to the look-back warps.
 //                      Verification tiles (sorted / reversed fast paths) are
 //                      checked here too.
-//   consumers (8)      once the look-back warp delivered a tile's offsets:
-//                      rank every key in its class with __ballot_sync /
-//                      __popc, stage the < run and the > run (records: also
-//                      the == payloads) in shared memory aligned like their
-//                      destinations, hand the stage back to the producer and
-//                      write the runs with cp.async.bulk stores (scalar
-//                      stores for the <= 3 unaligned keys at each end)
+//   consumers (8)      once the tile's offsets are known: keys to registers,
+//                      then (after a named barrier) restaged in place -- each
+//                      to its thread's next < slot or > slot, aligned like
+//                      the destination -- and written with cp.async.bulk
+//                      stores (scalar stores for the <= 3 unaligned keys at
+//                      each end); the stage is released once the stores
+//                      have read it
 #pragma once
 
 namespace tsq {

@@ -6,22 +6,23 @@
 //   partition_kernel   one recursion level over every live segment: the
 //                      multi-block three-way partition (the stage that
 //                      _run_machine performs, core.py:198-984).  Persistent,
-//                      warp-specialised: a producer warp claims tiles and
-//                      streams them into a 3-deep shared-memory ring with
-//                      bulk copies (TMA engine, cp.async.bulk + mbarrier);
-//                      8 consumer warps classify keys with __ballot_sync /
-//                      __popc, publish per-tile (<, >) counts and resolve
-//                      their offsets by decoupled look-back, then write the
+//                      warp-specialised (tsq_partition.cuh): a producer warp
+//                      streams tiles into a 6-deep shared-memory ring with
+//                      cp.async.bulk (TMA engine) + mbarriers; counter warps
+//                      count each consumer thread's < / > keys; look-back
+//                      warps turn tile counts into output offsets; consumer
+//                      warps restage each tile in output order and write the
 //                      < run from the segment front and the > run from the
 //                      back.  Segments whose samples looked sorted/reversed
 //                      are verified instead (core.py:1678-1698 fast paths).
-//   schedule_kernel    one warp per segment of the level: retires the ==p
-//                      run, samples the children's pivots (pivot.py:205-248)
-//                      and queues them for the next level or the on-chip
-//                      sort (core.py:1711-1728); the last CTA advances the
-//                      level and sets the CUDA-graph loop condition
-//   small_sort_kernel  on-chip sorting network for segments <= small_t
-//                      (insertion_sort's role, smallsort.py:12-47)
+//   schedule_kernel    one warp (or CTA) per child of each segment of the
+//                      level: retires the ==p run, samples the children's
+//                      pivots (pivot.py:205-248) and queues them for the next
+//                      level or the on-chip sort (core.py:1711-1728); the last
+//                      CTA advances the level and sets the CUDA-graph loop
+//                      condition
+//   small_sort_kernel  on-chip sort of segments <= small_t (insertion_sort's
+//                      role, smallsort.py:12-47): warp bitonic + merge path
 //   retire_kernel      writes ==p runs and verified runs into buffer 0
 //
 // Buffers: keys[0] is the caller's array (raw encoding), keys[1] the
@@ -139,12 +140,6 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
   }
   if (threadIdx.x == 0 && pv.use_cond) cudaGraphSetConditional(pv.cond, more ? 1u : 0u);
 }
-
-// ---------------------------------------------------------------------------
-// On-chip sort of segments <= small_t: bitonic sorting network in shared
-// memory (records sort (key, local index) pairs so equal keys keep distinct
-// payloads; padding sorts last).  Output always lands in buffer 0.
-
 
 // Retire finished runs into buffer 0, chunk by chunk.
 constexpr int kRB = 8;  // loads in flight per thread

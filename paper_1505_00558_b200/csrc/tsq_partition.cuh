@@ -6,25 +6,18 @@
 // < p sits at the segment front, every key > p at the back, and the == p
 // block (retired, never compared again) in between (core.py:944-967).
 //
-// Persistent CTAs, warp-specialised (320 threads):
-//   warp 8  producer   claims a tile (one atomic ticket) as soon as a stage of
-//                      the 4-deep shared-memory ring is free, resolves its
-//                      segment, and streams it in with cp.async.bulk (TMA
-//                      engine) completing on the stage's mbarrier
-//   warp 9  look-back  for each stage in order: once the consumers published
-//                      the tile's (<, >) aggregate, resolves the tile's
-//                      exclusive prefix in its segment by decoupled look-back
-//                      over the segment's earlier tiles and publishes the
-//                      inclusive prefix
-//   warps 0-7 consumers  software-pipelined by one tile: classify tile k+1
-//                      (every key against the pivot, ranked in its class with
-//                      __ballot_sync / __popc) and publish its aggregate,
-//                      then stage tile k's < run and > run (and, for records,
-//                      its == payloads) in shared memory aligned like their
-//                      destinations and write them with cp.async.bulk stores
-//                      (scalar stores for the <= 3 unaligned keys at each end)
-// The one-tile skew gives every look-back a full tile of consumer work to
-// complete in, so the consumers rarely wait for offsets.
+// Persistent CTAs (2 per SM), warp-specialised (480 threads):
+//   warp 8       producer: deals tiles round-robin, resolves their segments
+//                32 at a time, streams each into a 6-deep shared-memory ring
+//                with cp.async.bulk (TMA engine) completing on the stage's
+//                mbarrier; a DONE marker ends the ring
+//   warps 11-14  counters (tsq_consume.cuh): per consumer thread the (<, >)
+//                counts of its keys and their lane prefixes; tile aggregate
+//   warps 9-10   look-back: the tile's output offsets in its segment -- one
+//                atomic range reservation, or (reproducible mode) decoupled
+//                look-back over the segment's earlier tiles
+//   warps 0-7    consumers (tsq_consume.cuh): restage the tile in place in
+//                output order and write the < and > runs with cp.async.bulk
 #pragma once
 
 namespace tsq {
