@@ -50,8 +50,10 @@ class GpuConfig:
                  reversed (the _sorted_handler / _reversed_handler role,
                  core.py:991-1556); results are identical either way.
     max_depth    depth guard; exceeding it raises instead of degrading.
-    small_threshold  segments of at most this many keys (<= 8192) finish in the
-                 on-chip sort; 0 = 8192 for 4-byte keys, 4096 for 8-byte keys
+    small_threshold  segments of at most this many keys finish in the on-chip
+                 sort; 0 = the measured default (4-byte keys 16384, 4-byte
+                 records 8192, 8-byte keys 8192, 8-byte records 4096); values
+                 above the key type's on-chip capacity are clamped to it
                  (lower it to drive the partition machine on tiny inputs, like
                  the reference tests' insertion_threshold=3)
     host_levels  drive recursion levels from the host with a per-level trace
@@ -73,8 +75,8 @@ class GpuConfig:
     reproducible: bool = False
 
     def __post_init__(self):
-        if not (self.small_threshold == 0 or 1 <= self.small_threshold <= 8192):
-            raise ValueError("small_threshold must be 0 (auto) or in [1, 8192]")
+        if not (self.small_threshold == 0 or 1 <= self.small_threshold <= 16384):
+            raise ValueError("small_threshold must be 0 (auto) or in [1, 16384]")
         if not 8 <= self.max_depth <= 190:
             raise ValueError("max_depth must be in [8, 190]")
 

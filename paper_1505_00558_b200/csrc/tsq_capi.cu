@@ -18,11 +18,28 @@ using namespace tsq;
 namespace {
 
 struct KernelSet {
-  const void *init, *part, *sched, *small, *retire, *selp;
+  const void *init, *part, *sched, *retire, *selp;
   int key_bytes, tile;
-  size_t part_smem, sched_smem, small_smem, small2_smem;
-  const void *small2;  // 512-thread on-chip sort (segments of kSmallT+1 .. kSmallMax)
+  size_t part_smem, sched_smem;
+  // on-chip sort classes: 256 / 512 threads (tsq_small.cuh)
+  const void *small[kSmallClasses];
+  size_t small_smem[kSmallClasses];
+  int small_threads[kSmallClasses];
+  int small_cap[kSmallClasses];  // keys each class takes
+  int default_small_t;
 };
+
+int key_bytes_of(int dt);
+
+// Default on-chip cut (measured on B200 at the BASELINE sizes): 4-byte keys
+// the two-chunk 512-thread class's 16384 (records 8192), 8-byte keys 8192,
+// 8-byte records 4096 -- an on-chip merge round costs less than the
+// partition level it replaces until the sort items outgrow the class.
+int default_small_t(int kt, int pt) {
+  const bool pay = pt == TSQ_U32;
+  if (key_bytes_of(kt) == 4) return pay ? kSmallMax : kSmallHuge;
+  return pay ? kSmallT : kSmallMax;
+}
 
 template <int DT, bool PAY>
 KernelSet make_set() {
@@ -32,21 +49,20 @@ KernelSet make_set() {
   s.init = reinterpret_cast<const void *>(&init_kernel<C, PAY>);
   s.part = reinterpret_cast<const void *>(&partition_kernel<C, PAY>);
   s.sched = reinterpret_cast<const void *>(&schedule_kernel<C, PAY>);
-  s.small = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, kThreads>);
-  s.small2 = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 2 * kThreads>);
+  s.small[0] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, kThreads>);
+  s.small[1] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 2 * kThreads>);
+  s.small_smem[0] = SmallGeo<C, PAY, kThreads>::SMEM;
+  s.small_smem[1] = SmallGeo<C, PAY, 2 * kThreads>::SMEM;
+  for (int c = 0; c < kSmallClasses; ++c) s.small_threads[c] = kThreads << c;
+  s.small_cap[0] = SmallGeo<C, PAY, kThreads>::CAP;
+  s.small_cap[1] = SmallGeo<C, PAY, 2 * kThreads>::CAP;
+  s.default_small_t = default_small_t(DT, PAY ? TSQ_U32 : TSQ_NONE);
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
   s.key_bytes = (int)sizeof(U);
   s.tile = Geo<C, PAY>::TILE;
   s.part_smem = Geo<C, PAY>::SMEM;
   s.sched_smem = (size_t)(kThreads / 32) * (kMaxSample + 1) * sizeof(U);
-  // two padded-row merge buffers (+ index arrays), see tsq_small.cuh
-  {
-    typedef MergeTraits<Codec<DT>, PAY> M;
-    const size_t np = (size_t)kSmallT + (kSmallT >> kLogVT);
-    s.small_smem = 2 * np * sizeof(typename M::K) + (M::kIdx ? 2 * np * 4 : 0);
-    s.small2_smem = 2 * s.small_smem;
-  }
   return s;
 }
 
@@ -55,6 +71,11 @@ bool get_set(int dt, bool pay, KernelSet *out) {
   case D:                                                    \
     *out = pay ? make_set<D, true>() : make_set<D, false>(); \
     return true;
+#ifdef TSQ_ONLY  // experiment builds (scripts/variants.py): one (dtype, payload) set only
+  if (dt * 2 + (pay ? 1 : 0) != TSQ_ONLY) return false;
+  *out = make_set<TSQ_ONLY / 2, (TSQ_ONLY & 1) != 0>();
+  return true;
+#endif
   switch (dt) {
     TSQ_CASE(TSQ_I32)
     TSQ_CASE(TSQ_U32)
@@ -92,13 +113,14 @@ u64 host_enc(int dt, u64 x) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t keys_alt, pay_alt, side_pay, segs[2], tilemap[2], lookback[2], smalls, bigs, runs,
+  size_t keys_alt, pay_alt, side_pay, segs[2], tilemap[2], lookback[2], sq[kSmallClasses], runs,
       chunkmap;
   size_t total;
-  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap, big_cap;
+  uint32_t seg_cap, tile_cap, run_cap, chunk_cap, sq_cap[kSmallClasses];
 };
 
-Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallMax) {
+Layout make_layout(size_t n, int kt, int pt, int small_t = 0) {
+  if (small_t <= 0) small_t = default_small_t(kt, pt);
   Layout L;
   memset(&L, 0, sizeof(L));
   const int kb = key_bytes_of(kt);
@@ -107,8 +129,8 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallMax) {
   L.seg_cap = (uint32_t)(n / (size_t)small_t + 2);
   L.tile_cap = (uint32_t)(n / tile + 2ull * L.seg_cap + 2);
   L.run_cap = 8u * L.seg_cap + 64u;
-  L.small_cap = 2u * L.run_cap;
-  L.big_cap = (uint32_t)(n / (size_t)(kSmallT + 1) + 2);
+  L.sq_cap[0] = 2u * L.run_cap;
+  L.sq_cap[1] = (uint32_t)(n / (size_t)(kSmallT + 1) + 2);
   L.chunk_cap = (uint32_t)(n / kRunChunk + L.run_cap + 2);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -122,8 +144,7 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = kSmallMax) {
   for (int b = 0; b < 2; ++b) L.segs[b] = take((size_t)L.seg_cap * sizeof(Seg));
   for (int b = 0; b < 2; ++b) L.tilemap[b] = take((size_t)L.tile_cap * 4);
   for (int b = 0; b < 2; ++b) L.lookback[b] = take((size_t)L.tile_cap * 8);
-  L.smalls = take((size_t)L.small_cap * sizeof(SmallSeg));
-  L.bigs = take((size_t)L.big_cap * sizeof(SmallSeg));
+  for (int c = 0; c < kSmallClasses; ++c) L.sq[c] = take((size_t)L.sq_cap[c] * sizeof(SmallSeg));
   L.runs = take((size_t)L.run_cap * sizeof(Run));
   L.chunkmap = take((size_t)L.chunk_cap * 4);
   L.total = off;
@@ -182,8 +203,8 @@ int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem, int block = k
 }
 
 tsq_status prepare_small_smem(const KernelSet &ks) {
-  const void *fns[4] = {ks.part, ks.sched, ks.small, ks.small2};
-  const size_t sm[4] = {ks.part_smem, ks.sched_smem, ks.small_smem, ks.small2_smem};
+  const void *fns[4] = {ks.part, ks.sched, ks.small[0], ks.small[1]};
+  const size_t sm[4] = {ks.part_smem, ks.sched_smem, ks.small_smem[0], ks.small_smem[1]};
   // always opt in: dynamic + static shared memory may cross 48 KB even when
   // the dynamic part alone does not
   for (int i = 0; i < 4; ++i)
@@ -232,14 +253,14 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
     p->tilemap[b] = reinterpret_cast<uint32_t *>(base + L.tilemap[b]);
     p->lookback[b] = reinterpret_cast<u64 *>(base + L.lookback[b]);
   }
-  p->smalls = reinterpret_cast<SmallSeg *>(base + L.smalls);
-  p->bigs = reinterpret_cast<SmallSeg *>(base + L.bigs);
-  p->big_cap = L.big_cap;
+  for (int c = 0; c < kSmallClasses; ++c) {
+    p->sq[c] = reinterpret_cast<SmallSeg *>(base + L.sq[c]);
+    p->sq_cap[c] = L.sq_cap[c];
+  }
   p->runs = reinterpret_cast<Run *>(base + L.runs);
   p->chunkmap = reinterpret_cast<uint32_t *>(base + L.chunkmap);
   p->seg_cap = L.seg_cap;
   p->tile_cap = L.tile_cap;
-  p->small_cap = L.small_cap;
   p->run_cap = L.run_cap;
   p->chunk_cap = L.chunk_cap;
   p->ctl = ws->d_ctl;
@@ -247,7 +268,9 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
   p->fast_paths = 1;
   p->mitigation = 1;
   p->dran = 1.0;
-  p->small_t = kSmallMax;
+  p->small_t = kSmallHuge;
+  p->sq_lim[0] = kSmallT;
+  p->sq_lim[1] = kSmallHuge;
   p->reproducible = 0;
 }
 
@@ -259,7 +282,7 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   for (int i = 0; i < 4; ++i) TSQ_CUDA(cudaEventCreate(&ge->ev[i]));
   TSQ_CUDA(cudaGraphCreate(&ge->graph, 0));
   cudaGraph_t g = ge->graph;
-  cudaGraphNode_t e0, e1, e2, e3, cnode, lnode, snode, rnode;
+  cudaGraphNode_t e0, e1, e2, e3, cnode, lnode, rnode;
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e0, g, nullptr, 0, ge->ev[0]));
 
   static Params dummy;  // replaced per call via cudaGraphExecKernelNodeSetParams
@@ -308,30 +331,27 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   TSQ_CUDA(cudaGraphAddKernelNode(&schednode, body, &lnode, 1, &lk));
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e2, g, &cnode, 1, ge->ev[2]));
 
-  cudaKernelNodeParams sk = lk;
-  sk.func = const_cast<void *>(ks.small);
-  sk.gridDim = dim3(occupancy_grid(ws, ks.small, ks.small_smem));
-  sk.sharedMemBytes = (unsigned)ks.small_smem;
-  TSQ_CUDA(cudaGraphAddKernelNode(&snode, g, &e2, 1, &sk));
-  cudaKernelNodeParams sk2 = lk;
-  sk2.func = const_cast<void *>(ks.small2);
-  sk2.gridDim = dim3(occupancy_grid(ws, ks.small2, ks.small2_smem, 2 * kThreads));
-  sk2.blockDim = dim3(2 * kThreads);
-  sk2.sharedMemBytes = (unsigned)ks.small2_smem;
-  cudaGraphNode_t snode2;
-  TSQ_CUDA(cudaGraphAddKernelNode(&snode2, g, &e2, 1, &sk2));
+  cudaGraphNode_t tail[kSmallClasses + 1];
+  for (int c = 0; c < kSmallClasses; ++c) {
+    cudaKernelNodeParams sk = lk;
+    sk.func = const_cast<void *>(ks.small[c]);
+    sk.gridDim = dim3(occupancy_grid(ws, ks.small[c], ks.small_smem[c], ks.small_threads[c]));
+    sk.blockDim = dim3(ks.small_threads[c]);
+    sk.sharedMemBytes = (unsigned)ks.small_smem[c];
+    TSQ_CUDA(cudaGraphAddKernelNode(&tail[c], g, &e2, 1, &sk));
+  }
   cudaKernelNodeParams rk = lk;
   rk.func = const_cast<void *>(ks.retire);
   rk.gridDim = dim3(occupancy_grid(ws, ks.retire, 0));
   rk.sharedMemBytes = 0;
   TSQ_CUDA(cudaGraphAddKernelNode(&rnode, g, &e2, 1, &rk));
-  cudaGraphNode_t tail[3] = {snode, snode2, rnode};
-  TSQ_CUDA(cudaGraphAddEventRecordNode(&e3, g, tail, 3, ge->ev[3]));
+  tail[kSmallClasses] = rnode;
+  TSQ_CUDA(cudaGraphAddEventRecordNode(&e3, g, tail, kSmallClasses + 1, ge->ev[3]));
   TSQ_CUDA(cudaGraphInstantiate(&ge->exec, g, 0));
   return TSQ_OK;
 }
 
-tsq_status reserve_locked(tsq_workspace *ws, size_t n, int kt, int pt, int small_t = kSmallMax) {
+tsq_status reserve_locked(tsq_workspace *ws, size_t n, int kt, int pt, int small_t = 0) {
   const Layout L = make_layout(n, kt, pt, small_t);
   if (L.total <= ws->block_bytes) {
     if (n > ws->cap_elems) ws->cap_elems = n;
@@ -382,7 +402,8 @@ tsq_status fill_stats(tsq_workspace *ws, size_t n, tsq_stats *st) {
   st->stages = c.stages;
   st->levels = c.levels;
   st->max_depth = c.max_depth;
-  st->small_segments = (u64)c.small_count + (u64)c.big_count;
+  st->small_segments = 0;
+  for (int q = 0; q < kSmallClasses; ++q) st->small_segments += c.sq_count[q];
   st->eq_runs = c.eq_runs;
   st->eq_elements = c.eq_elements;
   st->sorted_bypass = c.sorted_bypass;
@@ -531,21 +552,23 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     if (stats) stats->n = n;
     return TSQ_OK;
   }
-  // default cut: the 512-thread class pays for 4-byte keys; 8-byte keys fit
-  // its shared memory only one CTA per SM, so they stop at the 256 class
-  int small_t = key_bytes_of(key_t) == 4 ? kSmallMax : kSmallT;
-  if (params && params->small_threshold > 0)
-    small_t = params->small_threshold < kSmallMax ? params->small_threshold : kSmallMax;
-  // allocation precedes any mutation (core.py:1599, TempAllocationError)
-  st = reserve_locked(ws, n, key_t, payload_t, small_t);
-  if (st != TSQ_OK) return st;
   const bool pay = payload_t == TSQ_U32;
   KernelSet ks;
   if (!get_set(key_t, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
+  int small_t = ks.default_small_t;
+#ifdef TSQ_SMALL_T
+  small_t = TSQ_SMALL_T;
+#endif
+  if (params && params->small_threshold > 0)
+    small_t = params->small_threshold < ks.small_cap[1] ? params->small_threshold : ks.small_cap[1];
+  // allocation precedes any mutation (core.py:1599, TempAllocationError)
+  st = reserve_locked(ws, n, key_t, payload_t, small_t);
+  if (st != TSQ_OK) return st;
   const Layout L = make_layout(n, key_t, payload_t, small_t);
   Params pv;
   fill_params(ws, L, &pv, keys, payload, n);
   pv.small_t = small_t;
+  for (int c = 0; c < kSmallClasses; ++c) pv.sq_lim[c] = ks.small_cap[c];
   tsq_params defaults;
   memset(&defaults, 0, sizeof(defaults));
   defaults.mitigation = 1;
@@ -635,11 +658,10 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     ws->sched_ms.push_back(ms2);
     total_levels += ms + ms2;
   }
-  TSQ_CUDA(cudaLaunchKernel(ks.small, dim3(occupancy_grid(ws, ks.small, ks.small_smem)),
-                            dim3(kThreads), largs, ks.small_smem, s));
-  TSQ_CUDA(cudaLaunchKernel(ks.small2,
-                            dim3(occupancy_grid(ws, ks.small2, ks.small2_smem, 2 * kThreads)),
-                            dim3(2 * kThreads), largs, ks.small2_smem, s));
+  for (int c = 0; c < kSmallClasses; ++c)
+    TSQ_CUDA(cudaLaunchKernel(
+        ks.small[c], dim3(occupancy_grid(ws, ks.small[c], ks.small_smem[c], ks.small_threads[c])),
+        dim3(ks.small_threads[c]), largs, ks.small_smem[c], s));
   TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
                             largs, 0, s));
   TSQ_CUDA(cudaEventRecord(t1, s));

@@ -49,6 +49,8 @@ __device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T
 struct StageCounts {
   uint32_t w[kConsumerWarps][3];
   uint32_t t[kConsumers];
+  u64 x[kConsumerWarps];  // per consumer warp: exclusive (<, ==, >) prefix, 21 bits each
+  u64 tot;                // the tile's (<, ==, >) totals, same packing
 };
 
 // class of key x against the pivot: 0 <, 1 ==, 2 >, 3 outside the segment
@@ -89,10 +91,8 @@ __device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, 
   return lt | (gt << 10) | (va << 20);
 }
 
-// Per-stage scratch of the counter warps: each one's share of the tile's
-// (<, >, valid) totals and the count of warps done with the stage.
+// Per-stage scratch of the counter warps: how many are done with the stage.
 struct CounterShare {
-  uint32_t lt[kCounterWarps], gt[kCounterWarps], va[kCounterWarps];
   uint32_t finished;
 };
 
@@ -201,7 +201,6 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
           if (lane >= o) inc[j] += y;
         }
       }
-      uint32_t tl = 0, tg = 0, tv = 0;
 #pragma unroll
       for (int j = 0; j < kSlices; ++j) {
         const int w = cw * kSlices + j;
@@ -213,44 +212,54 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
           sc[s].w[w][1] = va - lt - gt;
           sc[s].w[w][2] = gt;
         }
-        tl += lt;
-        tg += gt;
-        tv += va;
-      }
-      if (lane == 0) {
-        cs[s].lt[cw] = tl;
-        cs[s].gt[cw] = tg;
-        cs[s].va[cw] = tv;
       }
     }
     __syncwarp();
+    // the last counter warp done with the stage hands it on
+    uint32_t last = 0;
     if (lane == 0) {
-      // the last counter warp done with the stage hands it on
       __threadfence_block();
-      const bool last = atomicAdd(&cs[s].finished, 1u) == kCounterWarps - 1;
-      if (last) {
-        __threadfence_block();
-        cs[s].finished = 0;
-        if (part) {
-          uint32_t tl = 0, tg = 0, tv = 0;
+      last = atomicAdd(&cs[s].finished, 1u) == kCounterWarps - 1 ? 1u : 0u;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      if (part) {
+        // consumer warps' (<, ==, >) counts -> exclusive prefixes and the
+        // tile totals (lanes 0..7, 21-bit fields), so a consumer thread
+        // reads its warp's offsets instead of summing the others'
+        u64 pk = 0;
+        if (lane < kConsumerWarps)
+          pk = (u64)ld_volatile32(&sc[s].w[lane][0]) |
+               ((u64)ld_volatile32(&sc[s].w[lane][1]) << 21) |
+               ((u64)ld_volatile32(&sc[s].w[lane][2]) << 42);
+        u64 inc = pk;
 #pragma unroll
-          for (int c = 0; c < kCounterWarps; ++c) {
-            tl += ld_volatile32(&cs[s].lt[c]);
-            tg += ld_volatile32(&cs[s].gt[c]);
-            tv += ld_volatile32(&cs[s].va[c]);
-          }
+        for (int o = 1; o < kConsumerWarps; o <<= 1) {
+          const u64 y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (lane < kConsumerWarps) sc[s].x[lane] = inc - pk;
+        const u64 tot = __shfl_sync(0xffffffffu, inc, kConsumerWarps - 1);
+        if (lane == 0) {
+          sc[s].tot = tot;
+          const uint32_t tl = (uint32_t)(tot & 0x1fffffull), tq = (uint32_t)((tot >> 21) & 0x1fffffull);
+          const uint32_t tg = (uint32_t)(tot >> 42);
           const u64 agg = ((u64)tl << 31) | (u64)tg;
           m.agg = agg;
-          m.eq_excl = tv - tl - tg;  // (the look-back warp turns it into a slot)
+          m.eq_excl = tq;  // (the look-back warp turns it into a slot)
           if (reproducible)
             st_volatile(&P->lookback[cur][t], (m.k == 0 ? kFlagInc : kFlagAgg) | agg);
           TSQ_MARK(level, t, 3);
         }
+      }
+      if (lane == 0) {
+        cs[s].finished = 0;
         // the look-back warps turn the aggregate into the tile's offsets
         mbar_arrive(&aggr[s]);
       }
-      mbar_arrive(&empty[s]);  // done reading the stage
     }
+    if (lane == 0) mbar_arrive(&empty[s]);  // done reading the stage
   }
 }
 
@@ -335,13 +344,11 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   uint32_t pay[G::IPT];
   load_keys<C, PAY>(sk, sp, tid, key, pay);
   const StageCounts &c = sc[s];
-  uint32_t w_lt = 0, w_eq = 0, w_gt = 0, t_lt = 0, t_eq = 0, t_gt = 0;
-#pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) {
-    const uint32_t a = c.w[w][0], b = c.w[w][1], d = c.w[w][2];
-    if (w < warp) { w_lt += a; w_eq += b; w_gt += d; }
-    t_lt += a; t_eq += b; t_gt += d;
-  }
+  const u64 xw = c.x[warp], tt = c.tot;
+  const uint32_t w_lt = (uint32_t)(xw & 0x1fffffull), w_eq = (uint32_t)((xw >> 21) & 0x1fffffull),
+                 w_gt = (uint32_t)(xw >> 42);
+  const uint32_t t_lt = (uint32_t)(tt & 0x1fffffull), t_eq = (uint32_t)((tt >> 21) & 0x1fffffull),
+                 t_gt = (uint32_t)(tt >> 42);
   const u64 ex = m.excl;
   const int sb = (int)m.buf, db = sb ^ 1;
   const bool src_raw = P->raw[sb] != 0, dst_raw = P->raw[db] != 0;

@@ -21,7 +21,9 @@ typedef unsigned long long u64;
 
 constexpr int kThreads = 256;        // every kernel: 8 warps per CTA
 constexpr int kSmallT = 4096;        // on-chip sort, 256-thread class (<= this)
-constexpr int kSmallMax = 8192;      // on-chip sort, 512-thread class; default cut
+constexpr int kSmallMax = 8192;      // on-chip sort, 512-thread class, 8-byte items
+constexpr int kSmallHuge = 16384;    // on-chip sort, 512-thread class, 4-byte keys only
+constexpr int kSmallClasses = 2;
 constexpr int kMaxSample = 1023;     // pivot sample size cap (2^10 - 1)
 constexpr int kRunChunk = 8192;      // elements per retire work item
 constexpr int kMaxLevels = 200;      // hard stop for the level loop
@@ -51,7 +53,7 @@ struct Seg {
   uint32_t fail;
 };
 
-// A segment of <= kSmallMax elements waiting for the on-chip sort.
+// A segment of <= kSmallHuge elements waiting for the on-chip sort.
 struct SmallSeg {
   long long begin;
   int len;
@@ -74,10 +76,11 @@ struct Ctl {
   u64 run_packed;         // (runs << 32) | chunks appended
   uint32_t cur_nseg, cur_ntiles;
   uint32_t level, tile_ticket;
-  uint32_t ctas_done, small_count;
-  uint32_t small_ticket, run_ticket;
-  uint32_t error, big_count;  // big_count: segments queued for the 512-thread sort
-  uint32_t big_ticket, pad0;
+  uint32_t ctas_done, run_ticket;
+  uint32_t error, pad0;
+  // on-chip sort queues, one per class (256 / 512 threads): appended
+  // segments, work tickets
+  uint32_t sq_count[kSmallClasses], sq_ticket[kSmallClasses];
   u64 stages, max_depth, levels, eq_runs, eq_elements;
   u64 sorted_bypass, reversed_bypass, verify_fallbacks;
   u64 partitioned_elements, small_elements;
@@ -104,11 +107,12 @@ struct Params {
   Seg *segs[2];
   uint32_t *tilemap[2];
   u64 *lookback[2];
-  SmallSeg *smalls;       // on-chip sort queue, <= kSmallT keys
-  SmallSeg *bigs;         // on-chip sort queue, (kSmallT, kSmallMax] keys
+  SmallSeg *sq[kSmallClasses];  // on-chip sort queues, one per class
+  int sq_lim[kSmallClasses];    // largest segment of each class
   Run *runs;
   uint32_t *chunkmap;
-  uint32_t seg_cap, tile_cap, small_cap, run_cap, chunk_cap, big_cap;
+  uint32_t sq_cap[kSmallClasses];
+  uint32_t seg_cap, tile_cap, run_cap, chunk_cap;
   Ctl *ctl;
   cudaGraphConditionalHandle cond;
 };
@@ -257,14 +261,23 @@ __device__ __forceinline__ void mbar_wait_sleep(u64 *bar, uint32_t parity) {
     if (NS > 0) __nanosleep(NS);
   }
 }
+#ifndef TSQ_SLEEP_COUNTER_NS
+#define TSQ_SLEEP_COUNTER_NS TSQ_SLEEP_NS
+#endif
+#ifndef TSQ_SLEEP_LB_NS
+#define TSQ_SLEEP_LB_NS TSQ_SLEEP_NS
+#endif
+#ifndef TSQ_SLEEP_CONSUMER_NS
+#define TSQ_SLEEP_CONSUMER_NS TSQ_SLEEP_NS
+#endif
 __device__ __forceinline__ void wait_full_consumer(u64 *bar, uint32_t parity) {
-  mbar_wait_sleep<TSQ_SLEEP_NS>(bar, parity);
+  mbar_wait_sleep<TSQ_SLEEP_COUNTER_NS>(bar, parity);
 }
 __device__ __forceinline__ void wait_aggr_lookback(u64 *bar, uint32_t parity) {
-  mbar_wait_sleep<TSQ_SLEEP_NS>(bar, parity);
+  mbar_wait_sleep<TSQ_SLEEP_LB_NS>(bar, parity);
 }
 __device__ __forceinline__ void wait_ready_consumer(u64 *bar, uint32_t parity) {
-  mbar_wait_sleep<TSQ_SLEEP_NS>(bar, parity);
+  mbar_wait_sleep<TSQ_SLEEP_CONSUMER_NS>(bar, parity);
 }
 __device__ __forceinline__ void wait_empty_producer(u64 *bar, uint32_t parity) {
   mbar_wait_sleep<TSQ_SLEEP_PRODUCER_NS>(bar, parity);
@@ -312,6 +325,11 @@ __device__ __forceinline__ u64 warp_sum64(u64 v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// on-chip class of a segment of len keys
+__device__ __forceinline__ int small_class(const Params *P, long long len) {
+  return len <= P->sq_lim[0] ? 0 : 1;
 }
 
 // ---- pivot sample size: ~sqrt(len), 2^k - 1 with k in [5, 10] -------------

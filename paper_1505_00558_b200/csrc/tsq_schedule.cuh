@@ -31,12 +31,12 @@ constexpr long long kCtaScheduleMin = 1ll << 20;
 __device__ __forceinline__ void append_small(const Params *P, long long begin, long long len,
                                              uint32_t buf) {
   Ctl *ctl = P->ctl;
-  const bool big = len > kSmallT;  // the 512-thread class
-  const uint32_t slot = atomicAdd(big ? &ctl->big_count : &ctl->small_count, 1u);
-  if (slot < (big ? P->big_cap : P->small_cap)) {
+  const int c = small_class(P, len);
+  const uint32_t slot = atomicAdd(&ctl->sq_count[c], 1u);
+  if (slot < P->sq_cap[c]) {
     SmallSeg s;
     s.begin = begin; s.len = (int)len; s.buf = (int)buf;
-    (big ? P->bigs : P->smalls)[slot] = s;
+    P->sq[c][slot] = s;
   } else {
     atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
   }
@@ -349,7 +349,7 @@ struct RoundShared {
   ReqLevel lv[kThreads / 32][2];
   ReqRun run[kThreads / 32];
   ReqSmall sm[kThreads / 32][2];
-  uint32_t lv_slot0, lv_tile0, run_slot0, run_chunk0, sm_slot0, bg_slot0;
+  uint32_t lv_slot0, lv_tile0, run_slot0, run_chunk0, sq_slot0[kSmallClasses];
 };
 
 // Warp mode: one task per warp, task = (segment, child); the child-0 warp
@@ -431,11 +431,11 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
   __syncthreads();
   // one claim per queue for the whole round
   if (threadIdx.x == 0) {
-    uint32_t nl = 0, nt = 0, nr = 0, nc = 0, ns = 0, nb = 0;
+    uint32_t nl = 0, nt = 0, nr = 0, nc = 0, nq[kSmallClasses] = {};
     for (int w = 0; w < kThreads / 32; ++w) {
       for (int c = 0; c < 2; ++c) {
         if (rs.lv[w][c].valid) { ++nl; nt += rs.lv[w][c].ntiles; }
-        if (rs.sm[w][c].valid) ++(rs.sm[w][c].len > kSmallT ? nb : ns);
+        if (rs.sm[w][c].valid) ++nq[small_class(P, rs.sm[w][c].len)];
       }
       if (rs.run[w].valid) { ++nr; nc += rs.run[w].nchunks; }
     }
@@ -458,29 +458,27 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         rs.run_slot0 = kDone;
       }
     }
-    if (ns) {
-      rs.sm_slot0 = atomicAdd(&ctl->small_count, ns);
-      if (rs.sm_slot0 + ns > P->small_cap) {
-        atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-        rs.sm_slot0 = kDone;
-      }
-    }
-    if (nb) {
-      rs.bg_slot0 = atomicAdd(&ctl->big_count, nb);
-      if (rs.bg_slot0 + nb > P->big_cap) {
-        atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-        rs.bg_slot0 = kDone;
+    for (int q = 0; q < kSmallClasses; ++q) {
+      if (nq[q]) {
+        rs.sq_slot0[q] = atomicAdd(&ctl->sq_count[q], nq[q]);
+        if (rs.sq_slot0[q] + nq[q] > P->sq_cap[q]) {
+          atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+          rs.sq_slot0[q] = kDone;
+        }
       }
     }
   }
   __syncthreads();
   // each warp writes its records at its offsets
   uint32_t lslot = rs.lv_slot0, ltile = rs.lv_tile0, rslot = rs.run_slot0;
-  uint32_t rchunk = rs.run_chunk0, sslot = rs.sm_slot0, bslot = rs.bg_slot0;
+  uint32_t rchunk = rs.run_chunk0;
+  uint32_t qslot[kSmallClasses];
+#pragma unroll
+  for (int q = 0; q < kSmallClasses; ++q) qslot[q] = rs.sq_slot0[q];
   for (int w = 0; w < warp; ++w) {
     for (int c = 0; c < 2; ++c) {
       if (rs.lv[w][c].valid) { ++lslot; ltile += rs.lv[w][c].ntiles; }
-      if (rs.sm[w][c].valid) ++(rs.sm[w][c].len > kSmallT ? bslot : sslot);
+      if (rs.sm[w][c].valid) ++qslot[small_class(P, rs.sm[w][c].len)];
     }
     if (rs.run[w].valid) { ++rslot; rchunk += rs.run[w].nchunks; }
   }
@@ -504,13 +502,13 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     }
     const ReqSmall &m = rs.sm[warp][c];
     if (m.valid) {
-      const bool big = m.len > kSmallT;
-      if ((big ? rs.bg_slot0 : rs.sm_slot0) != kDone && lane == 0) {
+      const int q = small_class(P, m.len);
+      if (rs.sq_slot0[q] != kDone && lane == 0) {
         SmallSeg s;
         s.begin = m.begin; s.len = (int)m.len; s.buf = (int)m.buf;
-        (big ? P->bigs : P->smalls)[big ? bslot : sslot] = s;
+        P->sq[q][qslot[q]] = s;
       }
-      ++(big ? bslot : sslot);
+      ++qslot[q];
     }
   }
   const ReqRun &q = rs.run[warp];

@@ -326,17 +326,42 @@ __device__ __forceinline__ int merge_thread(const K *S, const uint32_t *SI, int 
   return cnt;
 }
 
+// Class geometry.  MULT: 16-key output chunks per thread in a merge round
+// (the 512-thread class takes up to 16384 four-byte keys with two).
+// Single-buffer classes hold every merge round's outputs in registers and
+// write them back over the input after a barrier, so they need one padded
+// buffer instead of two -- that is what fits the two-chunk class and 8-byte
+// sort items into the 512-thread class's shared memory at 2 CTAs per SM.
+template <class C, bool PAY, int NT>
+struct SmallGeo {
+  typedef MergeTraits<C, PAY> M;
+  typedef typename M::K K;
+  static constexpr int CLASS = NT == kThreads ? 0 : 1;
+  static constexpr int MULT = (CLASS == 1 && !PAY && sizeof(typename C::U) == 4) ? 2 : 1;
+  static constexpr int CAP = NT * kVT * MULT;       // keys
+  static constexpr int NP = CAP + CAP / kVT;         // padded capacity (rows of kVT + 1)
+  static constexpr bool SINGLE =
+      NT == 2 * kThreads && (MULT > 1 || (sizeof(K) + (M::kIdx ? 4 : 0)) > 4);
+  static constexpr size_t SMEM = (SINGLE ? 1 : 2) * (size_t)NP * (sizeof(K) + (M::kIdx ? 4 : 0));
+};
+
 template <class C, bool PAY, int NT>
 __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &sm,
                                                unsigned char *smem) {
   typedef typename C::U U;
   typedef MergeTraits<C, PAY> M;
   typedef typename M::K K;
+  typedef SmallGeo<C, PAY, NT> SG;
   constexpr bool IDX = M::kIdx;
-  constexpr int NP = NT * kVT + NT;  // padded capacity (rows of kVT + 1)
-  // smem: buffers A, B [NP] of K | (records, 64-bit keys) index A, B [NP]
-  K *ka = reinterpret_cast<K *>(smem), *kb = ka + NP;  // current / other buffer
-  uint32_t *ia = reinterpret_cast<uint32_t *>(kb + NP), *ib = ia + (IDX ? NP : 0);
+  constexpr bool SINGLE = SG::SINGLE;
+  constexpr int NP = SG::NP;
+  constexpr int MULT = SG::MULT;
+  constexpr int LPT = kVT * MULT;  // keys per thread
+  // smem: buffers A, B [NP] of K | (records, 64-bit keys) index A, B [NP];
+  // single-buffer classes: A only
+  K *ka = reinterpret_cast<K *>(smem), *kb = SINGLE ? ka : ka + NP;  // current / other buffer
+  uint32_t *ia = reinterpret_cast<uint32_t *>(ka + (SINGLE ? NP : 2 * NP));
+  uint32_t *ib = SINGLE ? ia : ia + (IDX ? NP : 0);
   const int tid = threadIdx.x;
   const int len = sm.len;
   // threads holding items: whole warps (the warp sort covers 32 * kVT)
@@ -345,14 +370,14 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
   const bool raw = P->raw[sm.buf] != 0;
   // coalesced load into padded rows (sentinels complete the last rows): all
   // of a thread's loads issued before any is used, so their latencies overlap
-  U raw_k[kVT];
+  U raw_k[LPT];
 #pragma unroll
-  for (int q = 0; q < kVT; ++q) {
+  for (int q = 0; q < LPT; ++q) {
     const int i = tid + q * NT;
     raw_k[q] = i < len ? src[i] : U(0);
   }
 #pragma unroll
-  for (int q = 0; q < kVT; ++q) {
+  for (int q = 0; q < LPT; ++q) {
     const int i = tid + q * NT;
     if (i < rows * kVT) {
       K x;
@@ -367,46 +392,73 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
     }
   }
   __syncthreads();
-  // every warp sorts its 32 rows
-  if (tid < rows) {
+  // every warp sorts runs of 32 rows (row = tid, tid + NT, ...: warp-uniform)
+#pragma unroll 1
+  for (int row = tid; row < rows; row += NT) {
     K v[kVT];
     uint32_t vi[kVT];
 #pragma unroll
     for (int r = 0; r < kVT; ++r) {
-      v[r] = ka[tid * (kVT + 1) + r];
-      vi[r] = IDX ? ia[tid * (kVT + 1) + r] : 0u;
+      v[r] = ka[row * (kVT + 1) + r];
+      vi[r] = IDX ? ia[row * (kVT + 1) + r] : 0u;
     }
     warp_sort<K, IDX>(v, vi);
 #pragma unroll
     for (int r = 0; r < kVT; ++r) {
-      ka[tid * (kVT + 1) + r] = v[r];
-      if (IDX) ia[tid * (kVT + 1) + r] = vi[r];
+      ka[row * (kVT + 1) + r] = v[r];
+      if (IDX) ia[row * (kVT + 1) + r] = vi[r];
     }
   }
-  // merge rounds
+  // merge rounds: output chunk m of a thread is row tid + m * NT
   for (int R = 32 * kVT; R < len; R <<= 1) {
     __syncthreads();
-    if (tid * kVT < len) {
-      K out[kVT];
-      uint32_t oi[kVT];
-      const int cnt = merge_thread<K, IDX>(ka, ia, tid * kVT, R, len, out, oi);
+    K out[MULT][kVT];
+    uint32_t oi[MULT][kVT];
+    int cnt[MULT];
+#pragma unroll
+    for (int m = 0; m < MULT; ++m) {
+      const int o = (tid + m * NT) * kVT;
+      cnt[m] = o < len ? merge_thread<K, IDX>(ka, ia, o, R, len, out[m], oi[m]) : 0;
+    }
+    if (SINGLE) __syncthreads();  // every thread has read its inputs
+#pragma unroll
+    for (int m = 0; m < MULT; ++m) {
+      const int row = tid + m * NT;
 #pragma unroll
       for (int r = 0; r < kVT; ++r)
-        if (r < cnt) {
-          kb[tid * (kVT + 1) + r] = out[r];
-          if (IDX) ib[tid * (kVT + 1) + r] = oi[r];
+        if (r < cnt[m]) {
+          kb[row * (kVT + 1) + r] = out[m][r];
+          if (IDX) ib[row * (kVT + 1) + r] = oi[m][r];
         }
     }
-    K *tk = ka; ka = kb; kb = tk;
-    uint32_t *ti = ia; ia = ib; ib = ti;
+    if (!SINGLE) {
+      K *tk = ka; ka = kb; kb = tk;
+      uint32_t *ti = ia; ia = ib; ib = ti;
+    }
   }
   __syncthreads();
   U *dst = reinterpret_cast<U *>(P->keys[0]) + sm.begin;
   const bool dst_raw = P->raw[0] != 0;
-  if (PAY) {
+  if (PAY && SINGLE) {
     // payloads gathered by local index straight from the source (an L1/L2
-    // resident window) into the free merge buffer, all before any is written
-    // (the source may be buffer 0 itself)
+    // resident window) into registers, all before any is written (the
+    // source may be buffer 0 itself)
+    const uint32_t *ps = P->pay[sm.buf] + sm.begin;
+    uint32_t pv[LPT];
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      const int i = tid + q * NT;
+      pv[q] = i < len ? ps[M::kPack ? (uint32_t)ka[pidx(i)] : ia[pidx(i)]] : 0u;
+    }
+    __syncthreads();
+    uint32_t *pd = P->pay[0] + sm.begin;
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      const int i = tid + q * NT;
+      if (i < len) pd[i] = pv[q];
+    }
+  } else if (PAY) {
+    // the same through the free merge buffer
     const uint32_t *ps = P->pay[sm.buf] + sm.begin;
     uint32_t *stage = reinterpret_cast<uint32_t *>(kb);
     for (int i = tid; i < len; i += NT)
@@ -423,19 +475,19 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
 }
 
 // One CTA per queued segment (tickets).  NT = 256: the queue of segments of
-// <= kSmallT keys; NT = 512: the queue of kSmallT+1 .. kSmallMax keys.
+// <= kSmallT keys; NT = 512: kSmallT+1 .. the class capacity.
 template <class C, bool PAY, int NT>
 __global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : (PAY ? 1 : 2))
     small_sort_kernel(const Params *__restrict__ P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
   Ctl *ctl = P->ctl;
-  const bool big = NT != kThreads;
-  const uint32_t n_q = big ? ctl->big_count : ctl->small_count;
-  const uint32_t cap = big ? P->big_cap : P->small_cap;
+  constexpr int cls = SmallGeo<C, PAY, NT>::CLASS;
+  const uint32_t n_q = ctl->sq_count[cls];
+  const uint32_t cap = P->sq_cap[cls];
   const uint32_t count = n_q < cap ? n_q : cap;
-  const SmallSeg *q = big ? P->bigs : P->smalls;
-  uint32_t *ticket = big ? &ctl->big_ticket : &ctl->small_ticket;
+  const SmallSeg *q = P->sq[cls];
+  uint32_t *ticket = &ctl->sq_ticket[cls];
   uint64_t elems = 0;
   for (;;) {
     if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1u);

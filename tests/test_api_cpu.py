@@ -82,10 +82,10 @@ def test_sortconfig_validation_matches_reference():
         T.SortConfig(late_swap_byte_threshold=0)
     T.SortConfig(insertion_threshold=3)
     with pytest.raises(ValueError):
-        T.GpuConfig(small_threshold=8193)
+        T.GpuConfig(small_threshold=16385)
     with pytest.raises(ValueError):
         T.GpuConfig(small_threshold=-1)
-    assert T.GpuConfig().small_threshold == 0  # auto: 8192 / 4096 by key width
+    assert T.GpuConfig().small_threshold == 0  # auto: the measured per-type default
     with pytest.raises(ValueError):
         T.GpuConfig(max_depth=4)
 

@@ -1,0 +1,107 @@
+"""GPU parity around the on-chip sort classes (tsq_small.cuh): segments of
+<= 4096 keys (256-thread class) and 4097 .. 8192 four-byte keys (512-thread
+class) finish in shared memory with warp bitonic networks + merge-path
+rounds.  Sizes straddle every class boundary and the partition pass's tile
+sizes; the inputs cover the shapes the reference battery exercises
+(datagen.py:106-198): uniform, few distinct, all equal, sorted, reversed,
+organ pipe, sawtooth, two sorted runs, and -0.0 / NaN for floats.  Bar:
+bit-exact against the CPU oracle (oracle/), the reference's algorithm
+restated in C.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1505_00558_b200 as T
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SIZES32 = [4095, 4096, 4097, 5000, 8191, 8192, 8193, 12288, 16385, 32768, 65536, 200003]
+SIZES64 = [4095, 4096, 4097, 8192, 12000, 16385, 40000]
+
+
+def _shapes(n, rng, dtype):
+    dt = np.dtype(dtype)
+    if dt.kind == "f":
+        base = rng.standard_normal(n)
+    else:
+        info = np.iinfo(dt)
+        base = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+    i = np.arange(n)
+    return {
+        "uniform": base.astype(dt),
+        "few3": rng.integers(0, 3, n).astype(dt),
+        "few100": rng.integers(0, 100, n).astype(dt),
+        "equal": np.full(n, 7, dtype=dt),
+        "sorted": np.sort(base).astype(dt),
+        "reversed": np.sort(base)[::-1].astype(dt),
+        "organ": np.minimum(i, n - 1 - i).astype(dt),
+        "saw": (i % 517).astype(dt),
+        "two_runs": np.concatenate([np.sort(base[: n // 2]), np.sort(base[n // 2:])]).astype(dt),
+    }
+
+
+def _check(x, sorter):
+    d = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    st = sorter.sort_with_stats(d)
+    want = x.copy()
+    O.sort(want, seed=1, threads=4)
+    got = d.cpu().numpy()
+    assert got.tobytes() == want.tobytes()
+    return st
+
+
+@pytest.fixture(scope="module")
+def sorter(cuda_ok):
+    return T.Sorter(seed=3)
+
+
+@pytest.mark.parametrize("n", SIZES32)
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.float32])
+def test_onchip_4byte(sorter, n, dtype):
+    rng = np.random.default_rng(n * 7 + 1)
+    for name, x in _shapes(n, rng, dtype).items():
+        _check(x, sorter)
+
+
+@pytest.mark.parametrize("n", SIZES64)
+@pytest.mark.parametrize("dtype", [np.int64, np.uint64, np.float64])
+def test_onchip_8byte(sorter, n, dtype):
+    rng = np.random.default_rng(n * 11 + 5)
+    for name, x in _shapes(n, rng, dtype).items():
+        _check(x, sorter)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_onchip_float_total_order(sorter, dtype):
+    """-0.0 before +0.0, NaNs at the ends (the device's IEEE total order;
+    the reference comparator cannot order them, so only the order-preserving
+    encoding is checked here, against numpy on the encoded bits)."""
+    rng = np.random.default_rng(99)
+    n = 20000
+    x = rng.standard_normal(n).astype(dtype)
+    x[rng.choice(n, 500, replace=False)] = -0.0
+    x[rng.choice(n, 500, replace=False)] = 0.0
+    d = torch.from_numpy(x.copy()).cuda()
+    sorter.sort(d)
+    got = d.cpu().numpy()
+    ut = np.uint32 if dtype == np.float32 else np.uint64
+    bits = x.view(ut)
+    sign = np.array(1, dtype=ut) << ut(8 * x.itemsize - 1)
+    enc = np.where(bits & sign, ~bits, bits | sign)
+    want = np.sort(enc)
+    dec = np.where(want & sign, want & ~sign, ~want).astype(ut).view(dtype)
+    assert got.tobytes() == dec.tobytes()
+
+
+def test_onchip_whole_array_in_one_segment(sorter):
+    """n <= the on-chip cut: the root segment goes straight on chip."""
+    rng = np.random.default_rng(5)
+    for n in (2, 4096, 4097, 6000, 8192):
+        st = _check(rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32), sorter)
+        assert st.gpu["levels"] == 0
