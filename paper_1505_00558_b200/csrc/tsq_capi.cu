@@ -27,6 +27,7 @@ struct KernelSet {
   int small_threads[kSmallClasses];
   int small_cap[kSmallClasses];  // keys each class takes
   int default_small_t;
+  bool raw_order;  // the workspace buffer keeps the caller's encoding too
 };
 
 int key_bytes_of(int dt);
@@ -57,6 +58,7 @@ KernelSet make_set() {
   s.small_cap[0] = SmallGeo<C, PAY, kThreads>::CAP;
   s.small_cap[1] = SmallGeo<C, PAY, 2 * kThreads>::CAP;
   s.default_small_t = default_small_t(DT, PAY ? TSQ_U32 : TSQ_NONE);
+  s.raw_order = C::kRawOrder;
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
   s.key_bytes = (int)sizeof(U);
@@ -568,6 +570,7 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   Params pv;
   fill_params(ws, L, &pv, keys, payload, n);
   pv.small_t = small_t;
+  pv.raw[1] = ks.raw_order ? 1 : 0;
   for (int c = 0; c < kSmallClasses; ++c) pv.sq_lim[c] = ks.small_cap[c];
   tsq_params defaults;
   memset(&defaults, 0, sizeof(defaults));

@@ -53,15 +53,11 @@ struct StageCounts {
   u64 tot;                // the tile's (<, ==, >) totals, same packing
 };
 
-// class of key x against the pivot: 0 <, 1 ==, 2 >, 3 outside the segment
-template <typename U>
-__device__ __forceinline__ uint32_t key_class(U x, U piv, bool valid) {
-  return ((uint32_t)(x >= piv) + (uint32_t)(x > piv)) | (valid ? 0u : 3u);
-}
-
 // one consumer warp's keys of a stage, counted by a counter lane in the
 // order the consumer will rank them; FULL: the whole tile is the segment's
-template <class C, bool PAY, bool FULL>
+// RAWCMP: the stage holds the caller's encoding of a kRawOrder key type --
+// compare natively against the decoded pivot, no per-key re-encoding.
+template <class C, bool PAY, bool FULL, bool RAWCMP>
 __device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, int lane, bool raw,
                                                 typename C::U piv, int rlo, int rhi) {
   typedef typename C::U U;
@@ -74,15 +70,17 @@ __device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, 
     unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) {
-      const U x = raw ? C::enc(key[q]) : key[q];
+      const U x = RAWCMP ? key[q] : (raw ? C::enc(key[q]) : key[q]);
+      const bool below = RAWCMP ? C::rlt(x, piv) : x < piv;
+      const bool above = RAWCMP ? C::rlt(piv, x) : x > piv;
       if (FULL) {
-        lt += x < piv ? 1u : 0u;
-        gt += x > piv ? 1u : 0u;
+        lt += below ? 1u : 0u;
+        gt += above ? 1u : 0u;
       } else {
         const int idx = e0 + q;
         const bool valid = idx >= rlo && idx < rhi;
-        lt += (valid && x < piv) ? 1u : 0u;
-        gt += (valid && x > piv) ? 1u : 0u;
+        lt += (valid && below) ? 1u : 0u;
+        gt += (valid && above) ? 1u : 0u;
         va += valid ? 1u : 0u;
       }
     }
@@ -131,6 +129,7 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
     if (lane == 0 && cw == 0) TSQ_MARK(level, t, 2);
     const U *sk = in_k + (size_t)s * G::SLOT;
     const bool raw = P->raw[m.buf] != 0;
+    const bool rawcmp = C::kRawOrder && raw;
     const int rlo = (int)(m.lo - m.tstart), rhi = (int)(m.hi - m.tstart);
     const bool part = m.kind == KIND_PARTITION;
     if (!part) {
@@ -152,12 +151,19 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
           if (v + 1 < NV) k[VN] = sk[(v + 1) * VN];
           else if (m.has_next) k[VN] = gk[m.hi];
           else { have = false; k[VN] = k[VN - 1]; }
+          if (rawcmp) {
 #pragma unroll
-          for (int q = 0; q <= VN; ++q)
-            if (raw) k[q] = C::enc(k[q]);
+            for (int q = 0; q < VN; ++q)
+              if (q + 1 < VN || have)
+                bad |= asc ? C::rlt(k[q + 1], k[q]) : C::rlt(k[q], k[q + 1]);
+          } else {
 #pragma unroll
-          for (int q = 0; q < VN; ++q)
-            if (q + 1 < VN || have) bad |= asc ? (k[q] > k[q + 1]) : (k[q] < k[q + 1]);
+            for (int q = 0; q <= VN; ++q)
+              if (raw) k[q] = C::enc(k[q]);
+#pragma unroll
+            for (int q = 0; q < VN; ++q)
+              if (q + 1 < VN || have) bad |= asc ? (k[q] > k[q + 1]) : (k[q] < k[q + 1]);
+          }
         }
       } else if (!m.skip) {
         const bool asc = m.kind == KIND_VERIFY_ASC;
@@ -167,11 +173,15 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
           if (i + 1 < rhi) b = sk[i + 1];
           else if (m.has_next) b = reinterpret_cast<const U *>(P->keys[m.buf])[m.hi];
           else have = false;
-          if (raw) {
-            a = C::enc(a);
-            b = C::enc(b);
+          if (rawcmp) {
+            if (have) bad |= asc ? C::rlt(b, a) : C::rlt(a, b);
+          } else {
+            if (raw) {
+              a = C::enc(a);
+              b = C::enc(b);
+            }
+            if (have) bad |= asc ? (a > b) : (a < b);
           }
-          if (have) bad |= asc ? (a > b) : (a < b);
         }
       }
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&P->segs[cur][m.sid].fail, 1u);
@@ -180,14 +190,26 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
       // all counted first, then their lane scans interleaved
       const U piv = (U)m.pivot;
       uint32_t own[kSlices], inc[kSlices];
-      if (rlo == 0 && rhi == G::TILE) {
+      const bool whole = rlo == 0 && rhi == G::TILE;
+      if (rawcmp) {
+        const U pr = C::dec(piv);  // the pivot in the caller's encoding
+        if (whole) {
+#pragma unroll
+          for (int j = 0; j < kSlices; ++j)
+            own[j] = count_slice<C, PAY, true, true>(sk, cw * kSlices + j, lane, raw, pr, rlo, rhi);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kSlices; ++j)
+            own[j] = count_slice<C, PAY, false, true>(sk, cw * kSlices + j, lane, raw, pr, rlo, rhi);
+        }
+      } else if (whole) {
 #pragma unroll
         for (int j = 0; j < kSlices; ++j)
-          own[j] = count_slice<C, PAY, true>(sk, cw * kSlices + j, lane, raw, piv, rlo, rhi);
+          own[j] = count_slice<C, PAY, true, false>(sk, cw * kSlices + j, lane, raw, piv, rlo, rhi);
       } else {
 #pragma unroll
         for (int j = 0; j < kSlices; ++j)
-          own[j] = count_slice<C, PAY, false>(sk, cw * kSlices + j, lane, raw, piv, rlo, rhi);
+          own[j] = count_slice<C, PAY, false, false>(sk, cw * kSlices + j, lane, raw, piv, rlo, rhi);
       }
       // at most 32 * IPT = 512 per class: three 10-bit counts, scanned
       // across the lanes; each consumer thread gets its exclusive prefix
@@ -294,10 +316,13 @@ __device__ __forceinline__ void stage_keys(const typename C::U *key, const uint3
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) {
       const U kq = key[v * G::VN + q];
-      const U x = (MODE & 1) ? C::enc(kq) : kq;
+      // MODE 3 with a raw-order codec: native compare against the decoded pivot
+      constexpr bool RC = MODE == 3 && C::kRawOrder;
+      const U x = RC ? kq : ((MODE & 1) ? C::enc(kq) : kq);
       const U y = MODE == 2 ? C::dec(kq) : (MODE == 1 ? x : kq);
       const bool valid = FULL || (e0 + q >= rlo && e0 + q < rhi);
-      const bool is_lt = valid && x < piv, is_gt = valid && x > piv;
+      const bool is_lt = valid && (RC ? C::rlt(x, piv) : x < piv);
+      const bool is_gt = valid && (RC ? C::rlt(piv, x) : x > piv);
       if (PAY) {
         const uint32_t pos = is_lt ? plt : (is_gt ? pgt : peq);
         if (is_lt || is_gt) ok[pos] = y;
@@ -387,19 +412,23 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
     return;
   }
 #endif
+#define TSQ_STAGE stage_keys
   if (src_raw && dst_raw) {
-    if (full) stage_keys<C, PAY, true, 3>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
-    else stage_keys<C, PAY, false, 3>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    // raw-order codecs compare in the caller's encoding: the decoded pivot
+    const U pv3 = C::kRawOrder ? C::dec(piv) : piv;
+    if (full) TSQ_STAGE<C, PAY, true, 3>(key, pay, tid, pv3, rlo, rhi, plt, pgt, peq, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 3>(key, pay, tid, pv3, rlo, rhi, plt, pgt, peq, sk, sp);
   } else if (src_raw) {
-    if (full) stage_keys<C, PAY, true, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
-    else stage_keys<C, PAY, false, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    if (full) TSQ_STAGE<C, PAY, true, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
   } else if (dst_raw) {
-    if (full) stage_keys<C, PAY, true, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
-    else stage_keys<C, PAY, false, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    if (full) TSQ_STAGE<C, PAY, true, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
   } else {
-    if (full) stage_keys<C, PAY, true, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
-    else stage_keys<C, PAY, false, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    if (full) TSQ_STAGE<C, PAY, true, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
   }
+#undef TSQ_STAGE
   fence_proxy_async_smem();
   named_sync(1, kConsumers);
 #ifdef TSQ_EXP_STAGE

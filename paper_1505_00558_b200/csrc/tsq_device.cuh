@@ -136,18 +136,28 @@ __device__ __forceinline__ void trace_mark(uint32_t level, uint32_t t, int slot)
 
 // ---- order-preserving key codecs (native order -> unsigned order) ----------
 template <int DT> struct Codec;
+// kRawOrder: the caller's bits compare natively (signed / unsigned integer
+// compare), so both ping-pong buffers keep the caller's encoding and the
+// partition pass compares with rlt() -- no per-key re-encoding.  Floats
+// keep the order-preserving unsigned encoding in the workspace buffer.
 template <> struct Codec<TSQ_I32> {
   typedef uint32_t U;
+  static constexpr bool kRawOrder = true;
+  static __device__ __forceinline__ bool rlt(U a, U b) { return (int32_t)a < (int32_t)b; }
   static __device__ __forceinline__ U enc(U x) { return x ^ 0x80000000u; }
   static __device__ __forceinline__ U dec(U x) { return x ^ 0x80000000u; }
 };
 template <> struct Codec<TSQ_U32> {
   typedef uint32_t U;
+  static constexpr bool kRawOrder = true;
+  static __device__ __forceinline__ bool rlt(U a, U b) { return a < b; }
   static __device__ __forceinline__ U enc(U x) { return x; }
   static __device__ __forceinline__ U dec(U x) { return x; }
 };
 template <> struct Codec<TSQ_F32> {
   typedef uint32_t U;
+  static constexpr bool kRawOrder = false;
+  static __device__ __forceinline__ bool rlt(U a, U b) { return enc(a) < enc(b); }
   static __device__ __forceinline__ U enc(U x) {
     return x ^ ((0u - (x >> 31)) | 0x80000000u);
   }
@@ -157,16 +167,22 @@ template <> struct Codec<TSQ_F32> {
 };
 template <> struct Codec<TSQ_I64> {
   typedef u64 U;
+  static constexpr bool kRawOrder = true;
+  static __device__ __forceinline__ bool rlt(U a, U b) { return (long long)a < (long long)b; }
   static __device__ __forceinline__ U enc(U x) { return x ^ 0x8000000000000000ull; }
   static __device__ __forceinline__ U dec(U x) { return x ^ 0x8000000000000000ull; }
 };
 template <> struct Codec<TSQ_U64> {
   typedef u64 U;
+  static constexpr bool kRawOrder = true;
+  static __device__ __forceinline__ bool rlt(U a, U b) { return a < b; }
   static __device__ __forceinline__ U enc(U x) { return x; }
   static __device__ __forceinline__ U dec(U x) { return x; }
 };
 template <> struct Codec<TSQ_F64> {
   typedef u64 U;
+  static constexpr bool kRawOrder = false;
+  static __device__ __forceinline__ bool rlt(U a, U b) { return enc(a) < enc(b); }
   static __device__ __forceinline__ U enc(U x) {
     return x ^ ((0ull - (x >> 63)) | 0x8000000000000000ull);
   }

@@ -43,7 +43,10 @@ constexpr int kLookbackWarps = 2;                 // alternate stages between th
 constexpr int kCounterWarp = kLookbackWarp + kLookbackWarps;  // warps 11-14: counts
 constexpr int kCounterWarps = 4;
 constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps + kCounterWarps);
-constexpr int kStages = 6;                        // stage ring depth
+#ifndef TSQ_STAGES
+#define TSQ_STAGES 6
+#endif
+constexpr int kStages = TSQ_STAGES;               // stage ring depth
 constexpr int kAlign = 4;                         // bulk-copy element alignment
 constexpr int kOutPad = 16;                       // alignment slack of a restaged tile
 constexpr uint32_t kDone = 0xffffffffu;

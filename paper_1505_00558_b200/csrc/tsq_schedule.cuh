@@ -23,10 +23,16 @@ enum SchedStat {
   ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_COUNT
 };
 
-constexpr int kWarpSampleMax = 127;   // warp-mode sample cap (4 per lane)
+#ifndef TSQ_WARP_SAMPLES
+#define TSQ_WARP_SAMPLES 127
+#endif
+#ifndef TSQ_CTA_SCHED_MIN
+#define TSQ_CTA_SCHED_MIN (1ll << 20)
+#endif
+constexpr int kWarpSampleMax = TSQ_WARP_SAMPLES;  // warp-mode sample cap (4 per lane)
 // Segments of at least this many keys (on average) are scheduled by a whole
 // CTA per child; below it one warp per child.
-constexpr long long kCtaScheduleMin = 1ll << 20;
+constexpr long long kCtaScheduleMin = TSQ_CTA_SCHED_MIN;
 
 __device__ __forceinline__ void append_small(const Params *P, long long begin, long long len,
                                              uint32_t buf) {
