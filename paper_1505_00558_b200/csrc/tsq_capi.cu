@@ -26,19 +26,20 @@ struct KernelSet {
   size_t small_smem[kSmallClasses];
   int small_threads[kSmallClasses];
   int small_cap[kSmallClasses];  // keys each class takes
-  int default_small_t;
   bool raw_order;  // the workspace buffer keeps the caller's encoding too
 };
 
 int key_bytes_of(int dt);
 
-// Default on-chip cut (measured on B200 at the BASELINE sizes): 4-byte keys
-// the two-chunk 512-thread class's 16384 (records 8192), 8-byte keys 8192,
-// 8-byte records 4096 -- an on-chip merge round costs less than the
-// partition level it replaces until the sort items outgrow the class.
-int default_small_t(int kt, int pt) {
+// Default on-chip cut (measured on B200, scripts/variants.py and
+// scripts/thr_sweep.py): 4-byte keys the two-chunk 512-thread class's 16384
+// (8192 up to 2^21 keys, where fewer, larger segments would leave SMs idle;
+// records 8192), 8-byte keys 8192, 8-byte records 4096 -- an on-chip merge
+// round costs less than the partition level it replaces until the sort
+// items outgrow the class.
+int default_small_t(int kt, int pt, size_t n) {
   const bool pay = pt == TSQ_U32;
-  if (key_bytes_of(kt) == 4) return pay ? kSmallMax : kSmallHuge;
+  if (key_bytes_of(kt) == 4) return pay || n <= (1u << 21) ? kSmallMax : kSmallHuge;
   return pay ? kSmallT : kSmallMax;
 }
 
@@ -57,7 +58,6 @@ KernelSet make_set() {
   for (int c = 0; c < kSmallClasses; ++c) s.small_threads[c] = kThreads << c;
   s.small_cap[0] = SmallGeo<C, PAY, kThreads>::CAP;
   s.small_cap[1] = SmallGeo<C, PAY, 2 * kThreads>::CAP;
-  s.default_small_t = default_small_t(DT, PAY ? TSQ_U32 : TSQ_NONE);
   s.raw_order = C::kRawOrder;
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
@@ -122,7 +122,7 @@ struct Layout {
 };
 
 Layout make_layout(size_t n, int kt, int pt, int small_t = 0) {
-  if (small_t <= 0) small_t = default_small_t(kt, pt);
+  if (small_t <= 0) small_t = default_small_t(kt, pt, n);
   Layout L;
   memset(&L, 0, sizeof(L));
   const int kb = key_bytes_of(kt);
@@ -557,7 +557,7 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   const bool pay = payload_t == TSQ_U32;
   KernelSet ks;
   if (!get_set(key_t, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
-  int small_t = ks.default_small_t;
+  int small_t = default_small_t(key_t, payload_t, n);
 #ifdef TSQ_SMALL_T
   small_t = TSQ_SMALL_T;
 #endif
