@@ -71,8 +71,9 @@ typedef struct {
   int32_t max_depth;       /* depth guard; default 96 */
   int32_t host_levels;     /* 1 = drive levels from the host (debug/per-level stats) */
   int32_t small_threshold; /* segments <= this go on chip (1..16384); 0 = the default:
-                            * 4-byte keys 16384 (records 8192), 8-byte keys 8192
-                            * (records 4096); clamped to the key type's capacity */
+                            * 4-byte keys 16384 (8192 up to 2^21 keys; records 8192),
+                            * 8-byte keys and records 8192; clamped to the key type's
+                            * capacity */
   int32_t reproducible;    /* 1 = run-to-run identical layout (decoupled look-back);
                             * 0 = tiles reserve output ranges with one atomic (faster) */
   int64_t reserved[3];

@@ -51,9 +51,9 @@ class GpuConfig:
                  core.py:991-1556); results are identical either way.
     max_depth    depth guard; exceeding it raises instead of degrading.
     small_threshold  segments of at most this many keys finish in the on-chip
-                 sort; 0 = the measured default (4-byte keys 16384, 4-byte
-                 records 8192, 8-byte keys 8192, 8-byte records 4096); values
-                 above the key type's on-chip capacity are clamped to it
+                 sort; 0 = the measured default (4-byte keys 16384 -- 8192 up
+                 to 2^21 keys --, records and 8-byte keys 8192); values above
+                 the key type's on-chip capacity are clamped to it
                  (lower it to drive the partition machine on tiny inputs, like
                  the reference tests' insertion_threshold=3)
     host_levels  drive recursion levels from the host with a per-level trace

@@ -34,13 +34,13 @@ int key_bytes_of(int dt);
 // Default on-chip cut (measured on B200, scripts/variants.py and
 // scripts/thr_sweep.py): 4-byte keys the two-chunk 512-thread class's 16384
 // (8192 up to 2^21 keys, where fewer, larger segments would leave SMs idle;
-// records 8192), 8-byte keys 8192, 8-byte records 4096 -- an on-chip merge
-// round costs less than the partition level it replaces until the sort
-// items outgrow the class.
+// records 8192), 8-byte keys and records 8192 -- an on-chip merge round
+// costs less than the partition level it replaces until the sort items
+// outgrow the class.
 int default_small_t(int kt, int pt, size_t n) {
   const bool pay = pt == TSQ_U32;
   if (key_bytes_of(kt) == 4) return pay || n <= (1u << 21) ? kSmallMax : kSmallHuge;
-  return pay ? kSmallT : kSmallMax;
+  return kSmallMax;
 }
 
 template <int DT, bool PAY>

@@ -345,14 +345,20 @@ struct SmallGeo {
   static constexpr size_t SMEM = (SINGLE ? 1 : 2) * (size_t)NP * (sizeof(K) + (M::kIdx ? 4 : 0));
 };
 
-template <class C, bool PAY, int NT>
+// Sort items: keys only -> the key; records with 32-bit keys -> key << 32 |
+// local index; records with 64-bit keys -> (key - lo) << 14 | local index
+// when the segment's keys span less than 2^50 (PK64: one u64 compare per
+// step, like the 32-bit case), else (key, index) pairs in two arrays.
+template <class C, bool PAY, int NT, bool PK64>
 __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &sm,
-                                               unsigned char *smem) {
+                                               unsigned char *smem, u64 lo) {
   typedef typename C::U U;
   typedef MergeTraits<C, PAY> M;
   typedef typename M::K K;
   typedef SmallGeo<C, PAY, NT> SG;
-  constexpr bool IDX = M::kIdx;
+  constexpr bool IDX = M::kIdx && !PK64;
+  constexpr bool PACK = M::kPack || PK64;   // (key, index) packed in one u64
+  constexpr int SH = M::kPack ? 32 : 14;    // index bits below the key
   constexpr bool SINGLE = SG::SINGLE;
   constexpr int NP = SG::NP;
   constexpr int MULT = SG::MULT;
@@ -383,7 +389,7 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
       K x;
       if (i < len) {
         const U k = raw ? C::enc(raw_k[q]) : raw_k[q];
-        x = M::kPack ? (K)(((u64)k << 32) | (u64)i) : (K)k;
+        x = PACK ? (K)((((u64)k - lo) << SH) | (u64)i) : (K)k;
       } else {
         x = ~K(0);
       }
@@ -448,7 +454,8 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
       const int i = tid + q * NT;
-      pv[q] = i < len ? ps[M::kPack ? (uint32_t)ka[pidx(i)] : ia[pidx(i)]] : 0u;
+      pv[q] = i < len ? ps[PACK ? (uint32_t)((u64)ka[pidx(i)] & ((1ull << SH) - 1)) : ia[pidx(i)]]
+                      : 0u;
     }
     __syncthreads();
     uint32_t *pd = P->pay[0] + sm.begin;
@@ -462,14 +469,14 @@ __device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &
     const uint32_t *ps = P->pay[sm.buf] + sm.begin;
     uint32_t *stage = reinterpret_cast<uint32_t *>(kb);
     for (int i = tid; i < len; i += NT)
-      stage[i] = ps[M::kPack ? (uint32_t)ka[pidx(i)] : ia[pidx(i)]];
+      stage[i] = ps[PACK ? (uint32_t)((u64)ka[pidx(i)] & ((1ull << SH) - 1)) : ia[pidx(i)]];
     __syncthreads();
     uint32_t *pd = P->pay[0] + sm.begin;
     for (int i = tid; i < len; i += NT) pd[i] = stage[i];
   }
   for (int i = tid; i < len; i += NT) {
     const K x = ka[pidx(i)];
-    const U k = M::kPack ? (U)(x >> 32) : (U)x;
+    const U k = PACK ? (U)(lo + ((u64)x >> SH)) : (U)x;
     dst[i] = dst_raw ? C::dec(k) : k;
   }
 }
@@ -481,6 +488,7 @@ __global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : (PAY ? 1 
     small_sort_kernel(const Params *__restrict__ P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
+  __shared__ u64 s_range[2];
   Ctl *ctl = P->ctl;
   constexpr int cls = SmallGeo<C, PAY, NT>::CLASS;
   const uint32_t n_q = ctl->sq_count[cls];
@@ -496,7 +504,30 @@ __global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : (PAY ? 1 
     __syncthreads();
     if (t >= count) break;
     const SmallSeg sm = q[t];
-    small_sort_one<C, PAY, NT>(P, sm, smem_raw);
+    if constexpr (MergeTraits<C, PAY>::kIdx) {
+      // 64-bit keys with payloads: the segment's key range decides the item
+      // form (one u64 when it spans < 2^50, else key + index arrays)
+      typedef typename C::U U;
+      const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
+      const bool raw = P->raw[sm.buf] != 0;
+      u64 mn = ~0ull, mx = 0ull;
+      for (int i = threadIdx.x; i < sm.len; i += NT) {
+        const u64 k = (u64)(raw ? C::enc(src[i]) : src[i]);
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+      }
+      if (threadIdx.x == 0) { s_range[0] = ~0ull; s_range[1] = 0ull; }
+      __syncthreads();
+      atomicMin(&s_range[0], mn);
+      atomicMax(&s_range[1], mx);
+      __syncthreads();
+      const u64 lo = s_range[0], hi = s_range[1];
+      __syncthreads();
+      if (((hi - lo) >> 50) == 0) small_sort_one<C, PAY, NT, true>(P, sm, smem_raw, lo);
+      else small_sort_one<C, PAY, NT, false>(P, sm, smem_raw, 0ull);
+    } else {
+      small_sort_one<C, PAY, NT, false>(P, sm, smem_raw, 0ull);
+    }
     elems += (uint64_t)sm.len;
     __syncthreads();
   }

@@ -105,3 +105,32 @@ def test_onchip_whole_array_in_one_segment(sorter):
     for n in (2, 4096, 4097, 6000, 8192):
         st = _check(rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32), sorter)
         assert st.gpu["levels"] == 0
+
+
+@pytest.mark.parametrize("dtype", [np.int64, np.uint64, np.float64, np.int32, np.uint32])
+@pytest.mark.parametrize("n", [3000, 8192, 12000, 70001])
+def test_onchip_records_item_forms(sorter, dtype, n):
+    """Records: 64-bit keys sort as one packed u64 (key - segment min, index)
+    when a segment's keys span < 2^50, else as (key, index) pairs; full-range
+    keys, a narrow cluster and a mix of both exercise both forms (and the
+    32-bit keys' packed form).  Keys bit-exact, payload a permutation
+    consistent with the keys (BASELINE.json config 5)."""
+    from conftest import assert_records_consistent
+    rng = np.random.default_rng(n + 17)
+    dt = np.dtype(dtype)
+    if dt.kind == "f":
+        wide = rng.standard_normal(n) * 1e300
+        narrow = 1.0 + rng.integers(0, 50, n) * 1e-12
+    else:
+        info = np.iinfo(dt)
+        wide = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        narrow = rng.integers(0, 100, n).astype(dt) + (info.max // 2 if dt.kind == "u" else 0)
+    mixed = np.where(rng.random(n) < 0.5, wide, narrow)
+    for keys in (wide.astype(dt), narrow.astype(dt), mixed.astype(dt)):
+        pay = np.arange(n, dtype=np.uint32)
+        dk = torch.from_numpy(keys.copy()).cuda()
+        dp = torch.from_numpy(pay).cuda()
+        sorter.sort(T.Records(dk, dp))
+        want = keys.copy()
+        O.sort(want, seed=1, threads=4)
+        assert_records_consistent(keys, dk.cpu().numpy(), dp.cpu().numpy(), want)
