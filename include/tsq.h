@@ -20,6 +20,9 @@
  *                            given pivot, returning the stage bounds
  *   tsq_select_pivot      <- select_pivot (pivot.py:205-248): the device
  *                            pivot-sampling kernel on one segment
+ *   tsq_apply_permutation <- bigelem._apply / apply_permutation
+ *                            (bigelem.py:48-86): the late-swap move of
+ *                            large elements, one gather pass
  *
  * Conventions: plain pointers and sizes; `keys`/`payload` are DEVICE
  * pointers owned by the caller and sorted in place; work is enqueued on the
@@ -152,6 +155,13 @@ tsq_status tsq_select_pivot(const void *keys, size_t n, tsq_dtype key_t,
                             double dran, int32_t mitigation,
                             tsq_workspace *ws, void *stream,
                             uint64_t *pivot, int32_t *order_flag);
+
+/* Late swapping (bigelem.py:31-99): dst_rows[i] = src_rows[perm[i]] for n
+ * rows of row_bytes each (device pointers, distinct buffers; perm a device
+ * array of n uint32 origins, i.e. the payload of a (key, index) records
+ * sort).  Enqueued on `stream`, does not sync. */
+tsq_status tsq_apply_permutation(const void *src_rows, void *dst_rows, size_t n,
+                                 size_t row_bytes, const uint32_t *perm, void *stream);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,7 @@ from .config import DEFAULT_CONFIG, DEFAULT_GPU_CONFIG, GpuConfig, SortConfig
 from .core import (DepthExceededError, DeviceTempStore, Records, Sorter,
                    TempAllocationError, free_temp_storage, key_cmp, sort, sort_many,
                    sort_with_stats)
+from .bigelem import Permutation, apply_permutation, sort_indirect
 from .pivot import MitigationRng, rng_next
 from .stats import SortStats
 
@@ -37,7 +38,7 @@ def get_algorithm(name: str):
 
 __all__ = [
     "DEFAULT_CONFIG", "DEFAULT_GPU_CONFIG", "DepthExceededError", "DeviceTempStore",
-    "GpuConfig", "MitigationRng", "REGISTRY", "Records", "SortConfig", "SortStats", "Sorter",
-    "TempAllocationError", "free_temp_storage", "get_algorithm", "key_cmp", "rng_next",
-    "sort", "sort_many", "sort_with_stats",
+    "GpuConfig", "MitigationRng", "Permutation", "REGISTRY", "Records", "SortConfig", "SortStats",
+    "Sorter", "TempAllocationError", "apply_permutation", "free_temp_storage", "get_algorithm",
+    "key_cmp", "rng_next", "sort", "sort_indirect", "sort_many", "sort_with_stats",
 ]

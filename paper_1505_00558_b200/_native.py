@@ -22,7 +22,7 @@ EXPORTED_SYMBOLS = (
     "tsq_status_str", "tsq_abi_version", "tsq_workspace_create", "tsq_workspace_destroy",
     "tsq_workspace_bytes", "tsq_workspace_reserve", "tsq_workspace_free",
     "tsq_workspace_capacity", "tsq_workspace_alloc_count", "tsq_sort",
-    "tsq_partition_segment", "tsq_select_pivot", "tsq_level_trace",
+    "tsq_partition_segment", "tsq_select_pivot", "tsq_level_trace", "tsq_apply_permutation",
 )
 
 
@@ -103,6 +103,8 @@ def lib():
                                       ctypes.POINTER(ctypes.c_uint32),
                                       ctypes.POINTER(ctypes.c_uint64), i32]
         L.tsq_level_trace.restype = i32
+        L.tsq_apply_permutation.argtypes = [vp, vp, sz, sz, vp, vp]
+        L.tsq_apply_permutation.restype = i32
         _lib = L
     return _lib
 

@@ -59,7 +59,9 @@ def key_cmp(x, y) -> int:
 
 @dataclass
 class Records:
-    """Keys plus a uint32 payload that moves with its key."""
+    """Keys plus a payload that moves with its key: a uint32 vector (sorted
+    along on the device), or rows -- any tensor / array whose first
+    dimension is n -- moved once by late swapping (bigelem.py)."""
 
     keys: object
     payload: object
@@ -194,7 +196,20 @@ class Sorter:
         self.sort_with_stats(ar, cmp, element_size)
 
     def sort_with_stats(self, ar, cmp=None, element_size: int | None = None) -> SortStats:
-        """Sort ``ar`` in place on the GPU; returns the run's counters."""
+        """Sort ``ar`` in place on the GPU; returns the run's counters.
+
+        Elements of ``element_size >= config.late_swap_byte_threshold`` bytes
+        (and ``Records`` whose payload is a tensor of rows) take the late-swap
+        path: a device handle sort, then one gather pass over the elements
+        (bigelem.py, dispatched before the reentrancy guard as in
+        core.py:1595-1598)."""
+        late = (element_size is not None and
+                element_size >= self.config.late_swap_byte_threshold) or _rows_payload(ar)
+        if late and self._active:
+            raise RuntimeError("sorter instance is not reentrant")
+        if late and _length(ar) > 1:
+            from .bigelem import sort_large_elements
+            return sort_large_elements(ar, cmp, self)
         with self._lock:
             if self._active:
                 raise RuntimeError("sorter instance is not reentrant")
@@ -419,10 +434,6 @@ class Sorter:
         job.finish = finish
 
     def _sort(self, ar, cmp, element_size) -> SortStats:
-        if element_size is not None and element_size >= self.config.late_swap_byte_threshold:
-            raise NotImplementedError(
-                "late swapping (element_size >= late_swap_byte_threshold, bigelem.py) is "
-                "outside the GPU sort path")
         job = self._prepare(ar, cmp)
         stats = SortStats()
         if job.n <= 1:
@@ -457,6 +468,22 @@ class Sorter:
                     self.stage_hook(i, lv)
         job.finish()
         return _to_stats(ts, job)
+
+
+def _rows_payload(ar) -> bool:
+    """Records whose payload is not a 1-D uint32 vector: rows that move by
+    late swapping."""
+    if not isinstance(ar, Records):
+        return False
+    p = ar.payload
+    if isinstance(p, np.ndarray):
+        return p.ndim != 1 or p.dtype != np.uint32
+    torch = _torch()
+    return isinstance(p, torch.Tensor) and (p.dim() != 1 or p.dtype != torch.uint32)
+
+
+def _length(ar) -> int:
+    return len(ar.keys) if isinstance(ar, Records) else len(ar)
 
 
 def _to_stats(ts: N.TsqStats, job: _Job) -> SortStats:

@@ -223,7 +223,11 @@ struct LevelLaunch {
 LevelLaunch level_launch(tsq_workspace *ws, const KernelSet &ks) {
   LevelLaunch L;
   L.part_grid = dim3(occupancy_grid(ws, ks.part, ks.part_smem, kPartThreads));
+#ifdef TSQ_SCHED_PER_SM
+  L.sched_grid = dim3(TSQ_SCHED_PER_SM * ws->num_sms);
+#else
   L.sched_grid = dim3(occupancy_grid(ws, ks.sched, ks.sched_smem));
+#endif
   return L;
 }
 
@@ -782,6 +786,25 @@ tsq_status tsq_select_pivot(const void *keys, size_t n, tsq_dtype key_t, double 
   const int kb = key_bytes_of(key_t);
   *pivot = kb == 4 ? (ws->h_ctl->stage_lt & 0xffffffffull) : ws->h_ctl->stage_lt;
   *order_flag = (int32_t)(long long)ws->h_ctl->stage_gt;
+  return TSQ_OK;
+}
+
+tsq_status tsq_apply_permutation(const void *src_rows, void *dst_rows, size_t n,
+                                 size_t row_bytes, const uint32_t *perm, void *stream) {
+  if (n == 0 || row_bytes == 0) return TSQ_OK;
+  if (!src_rows || !dst_rows || !perm || src_rows == dst_rows) return TSQ_ERR_INVALID;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const uintptr_t a = (uintptr_t)src_rows | (uintptr_t)dst_rows | (uintptr_t)row_bytes;
+  int mode = (a % 16 == 0) ? 2 : ((a % 4 == 0) ? 1 : 0);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t want = (n + 7) / 8;  // 8 warps (rows in flight) per CTA
+  const unsigned grid = (unsigned)(want < (size_t)sms * 8 ? want : (size_t)sms * 8);
+  gather_rows_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const unsigned char *>(src_rows),
+                                          reinterpret_cast<unsigned char *>(dst_rows), perm, n,
+                                          row_bytes, mode);
+  TSQ_CUDA(cudaGetLastError());
   return TSQ_OK;
 }
 

@@ -91,6 +91,7 @@ struct StageMeta {
 #include "tsq_partition.cuh"
 #include "tsq_small.cuh"
 #include "tsq_schedule.cuh"
+#include "tsq_gather.cuh"
 
 namespace tsq {
 

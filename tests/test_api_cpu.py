@@ -126,13 +126,64 @@ def test_trivial_inputs_need_no_device():
         assert got == ar and st.comparisons == 0 and st.element_writes == 0
 
 
-def test_rejects_custom_comparator_and_late_swap_without_fallback():
+def test_rejects_custom_comparator_without_fallback():
     with pytest.raises(TypeError):
         T.Sorter().sort([3, 1, 2], cmp=lambda a, b: (a > b) - (a < b))
-    with pytest.raises(NotImplementedError):
-        T.Sorter().sort([3, 1, 2], element_size=400)
+    with pytest.raises(TypeError):  # the late-swap path has no comparator fallback either
+        T.Sorter().sort([3, 1, 2], cmp=lambda a, b: (a > b) - (a < b), element_size=400)
     with pytest.raises(TypeError):
         T.Sorter().sort(["a", "b", "c"])
+
+
+# ---- late swapping (bigelem.py): host-side permutation semantics -----------
+
+def test_apply_identity_zero_moves():
+    ar = list(range(5))
+    assert T.apply_permutation(ar, T.Permutation((0, 1, 2, 3, 4))) == 0
+    assert ar == [0, 1, 2, 3, 4]
+
+
+def test_apply_single_two_cycle():
+    ar = [1, 0, 2]
+    assert T.apply_permutation(ar, T.Permutation((1, 0, 2))) == 3
+    assert ar == [0, 1, 2]
+
+
+def test_apply_full_reversal_n6():
+    ar = [5, 4, 3, 2, 1, 0]
+    assert T.apply_permutation(ar, T.Permutation((5, 4, 3, 2, 1, 0))) == 9
+    assert ar == [0, 1, 2, 3, 4, 5]
+
+
+def test_permutation_length_mismatch():
+    with pytest.raises(ValueError):
+        T.apply_permutation([1, 2], T.Permutation((0, 1, 2)))
+
+
+def test_cycle_move_count_matches_reference_walk():
+    """moves = sum(c + 1) over nontrivial cycles (bigelem.py:48-76), from
+    the pointer-jumping cycle count, on random permutations."""
+    from paper_1505_00558_b200.bigelem import cycle_moves
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 2, 7, 64, 1000, 4097):
+        p = rng.permutation(n)
+        if n > 10:
+            p[: n // 3] = np.arange(n // 3)  # fixed points
+            p[n // 3:] = rng.permutation(np.arange(n // 3, n))
+        seen = np.zeros(n, bool)
+        want = cyc = 0
+        for i in range(n):
+            if seen[i]:
+                continue
+            c, j = 0, i
+            while not seen[j]:
+                seen[j] = True
+                j = p[j]
+                c += 1
+            if c > 1:
+                want += c + 1
+                cyc += 1
+        assert cycle_moves(p) == (want, cyc)
 
 
 def test_no_cpu_fallback_without_gpu():
