@@ -223,3 +223,23 @@ def test_workloads_generators_small():
         assert (p is None) == (not W.FAMILIES[fam][1])
     k, _ = W.generate("normal_f64", 100000)
     assert not np.isnan(k).any() and not (np.signbit(k) & (k == 0)).any()
+
+
+def test_battery_generators_match_reference():
+    """tests/battery.py (the reference's datagen restated) reproduces the
+    reference's own battery inputs (tests/golden/battery.json, written by
+    tests/golden/make_battery.py from tsqsort.datagen)."""
+    import hashlib
+    from battery import battery_cells, generate
+    from conftest import load_golden
+    g = load_golden("battery.json")
+    sha = lambda a: hashlib.sha256(np.asarray(a, dtype=np.int64).tobytes()).hexdigest()[:16]
+    sm = g["small"]
+    for d, r in battery_cells():
+        a = generate(d, r, sm["n"], sm["arange"], sm["seed"])
+        assert sha(a) == sm["cells"][f"{d}/{r}"], (d, r)
+    for key in ("random/fort", "shuffle/dither", "organpipes/reversed", "stagger/sorted"):
+        d, r = key.split("/")
+        a = generate(d, r, g["n"], g["arange"], g["seed"])
+        assert sha(a) == g["cells"][key]["input_sha"], key
+        assert sha(np.sort(a)) == g["cells"][key]["sorted_sha"], key
