@@ -116,13 +116,13 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
     u64 piv = pv.given_pivot;
     uint32_t kind = KIND_PARTITION, buf = pv.single_stage ? 1u : 0u;
     if (!pv.single_stage) {
-      __shared__ U s_piv;
-      __shared__ int s_flag;
-      cta_select_pivot<C>(reinterpret_cast<const U *>(pv.keys[0]), !pv.raw[0], 0, n, pv.dran,
-                          pv.mitigation, s_scr, &s_piv, &s_flag);
-      piv = (u64)s_piv;
+      // the register bitonic network of the schedule kernel's CTA mode
+      __shared__ uint32_t s_bc[2];
+      int flag = 0;
+      piv = (u64)cta_select_pivot_fast<C>(reinterpret_cast<const U *>(pv.keys[0]), !pv.raw[0], 0,
+                                          n, pv.dran, pv.mitigation, s_scr, s_bc, &flag);
       if (pv.fast_paths)
-        kind = s_flag > 0 ? KIND_VERIFY_ASC : (s_flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
+        kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
     }
     const uint32_t ntiles = (uint32_t)((n - 1) / T + 1);
     if (threadIdx.x == 0) {
