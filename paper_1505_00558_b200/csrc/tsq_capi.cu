@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -649,6 +650,10 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
       ws->level_bytes.push_back(ws->h_ctl->bytes_partition - bytes_before);
       bytes_before = ws->h_ctl->bytes_partition;
     }
+    if (getenv("TSQ_DEBUG_LEVELS"))
+      fprintf(stderr, "tsq level %d: segments %u tiles %u small %u/%u runs %u error %u\n", lv,
+              ws->h_ctl->cur_nseg, ws->h_ctl->cur_ntiles, ws->h_ctl->sq_count[0],
+              ws->h_ctl->sq_count[1], (uint32_t)(ws->h_ctl->run_packed >> 32), ws->h_ctl->error);
     if (ws->h_ctl->cur_nseg == 0 || ws->h_ctl->error) break;
     ws->level_segs.push_back(ws->h_ctl->cur_nseg);
     ws->level_tiles.push_back(ws->h_ctl->cur_ntiles);

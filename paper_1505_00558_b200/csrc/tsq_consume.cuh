@@ -357,7 +357,19 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   const uint32_t level = P->ctl->level;
   (void)level;
   if (m.kind != KIND_PARTITION) {
-    if (tid == 0) mbar_arrive(&empty[s]);  // verified by the counters: nothing to write
+    // verified by the counters: nothing to write.  The stage the last
+    // partition tile's bulk stores were reading is released here too --
+    // otherwise a run of verification tiles after a partition tile would
+    // leave it held until the next partition tile, and the producer,
+    // wrapping around the ring onto it, would stall the pipeline for good.
+    if (tid == 0) {
+      if (pend >= 0) {
+        bulk_wait_read0();
+        mbar_arrive(&empty[pend]);
+        pend = -1;
+      }
+      mbar_arrive(&empty[s]);
+    }
     return;
   }
   const uint32_t t = m.t;

@@ -134,3 +134,34 @@ def test_onchip_records_item_forms(sorter, dtype, n):
         want = keys.copy()
         O.sort(want, seed=1, threads=4)
         assert_records_consistent(keys, dk.cpu().numpy(), dp.cpu().numpy(), want)
+
+
+def test_verification_tiles_after_partition_tiles(cuda_ok):
+    """Regression: a level whose CTAs see a partition tile followed by many
+    verification tiles (sorted / reversed fast paths) -- a small random
+    segment next to a large sorted or reversed one, or thousands of 2-key
+    segments with small_threshold=1 -- must not stall the partition
+    pipeline (the stage held for the partition tile's bulk stores is
+    released by the verification tiles)."""
+    rng = np.random.default_rng(31)
+    for n in (1 << 20, 1 << 22):
+        for tail in ("asc", "desc"):
+            head = rng.integers(0, 1000, n // 4).astype(np.int32)
+            body = np.arange(1000, 1000 + n - n // 4, dtype=np.int32)
+            if tail == "desc":
+                body = body[::-1].copy()
+            x = np.concatenate([head, body])
+            d = torch.from_numpy(x.copy()).cuda()
+            T.Sorter(seed=1).sort(d)
+            assert d.cpu().numpy().tobytes() == np.sort(x).tobytes()
+    for dt in (np.int32, np.uint64):
+        for kind in ("random", "nearly"):
+            x = np.sort(rng.integers(0, 1 << 30, 20000).astype(dt))
+            if kind == "random":
+                rng.shuffle(x)
+            else:
+                a, b = rng.integers(0, x.size, 200), rng.integers(0, x.size, 200)
+                x[a], x[b] = x[b], x[a]
+            d = torch.from_numpy(x.copy()).cuda()
+            T.Sorter(seed=3, gpu=T.GpuConfig(small_threshold=1)).sort(d)
+            assert d.cpu().numpy().tobytes() == np.sort(x).tobytes()
