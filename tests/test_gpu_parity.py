@@ -358,3 +358,21 @@ def test_sort_many_pipeline(cuda_ok):
         T.sort_many([np.zeros(4, np.int32), np.zeros(4, np.int64)])
     with pytest.raises(TypeError):
         T.sort_many([torch.zeros(4, dtype=torch.int32, device="cuda")])
+
+
+@pytest.mark.parametrize("keydt", [np.uint64, np.uint32, np.float64])
+def test_reproducible_records_payload_order(cuda_ok, keydt):
+    """GpuConfig(reproducible=True): the decoupled look-back placement makes
+    every level's layout, and so the order of equal-key payloads, identical
+    run to run (C5-style heavy duplication, both on-chip item forms)."""
+    rng = np.random.default_rng(11)
+    n = 1 << 20
+    keys = rng.integers(0, 1 << 12, n).astype(keydt)
+    outs = []
+    for _ in range(2):
+        dk, dp = _dev(keys), _dev(np.arange(n, dtype=np.uint32))
+        T.Sorter(seed=5, gpu=T.GpuConfig(reproducible=True)).sort(T.Records(dk, dp))
+        outs.append((dk.cpu().numpy(), dp.cpu().numpy()))
+    assert outs[0][0].tobytes() == outs[1][0].tobytes() == np.sort(keys).tobytes()
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert_records_consistent(keys, outs[0][0], outs[0][1], np.sort(keys))
