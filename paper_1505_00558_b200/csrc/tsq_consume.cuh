@@ -113,8 +113,8 @@ __device__ __forceinline__ void counter_loop(const Params *P, int cur, const typ
   const uint32_t level = P->ctl->level;
   (void)level;
   for (uint32_t it = 0;; ++it) {
-    const int s = (int)(it % kStages);
-    wait_full_consumer(&full[s], (it / kStages) & 1u);
+    const int s = (int)(it % G::STAGES);
+    wait_full_consumer(&full[s], (it / G::STAGES) & 1u);
     StageMeta &m = meta[s];
     if (m.kind == KIND_DONE) {
       // out of tiles: the last counter warp here passes the marker on
@@ -352,7 +352,7 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   typedef Geo<C, PAY> G;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int s = (int)(it % kStages);
+  const int s = (int)(it % G::STAGES);
   const StageMeta &m = meta[s];
   const uint32_t level = P->ctl->level;
   (void)level;
@@ -488,19 +488,19 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
   const Params *P = &sparams;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   U *in_k = reinterpret_cast<U *>(smem_raw);
-  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)kStages * G::SLOT);
-  __shared__ __align__(8) u64 full[kStages], aggr[kStages], ready[kStages], empty[kStages];
-  __shared__ StageMeta meta[kStages];
-  __shared__ StageCounts sc[kStages];
-  __shared__ CounterShare cshare[kStages];
+  uint32_t *in_p = reinterpret_cast<uint32_t *>(in_k + (size_t)G::STAGES * G::SLOT);
+  __shared__ __align__(8) u64 full[G::STAGES], aggr[G::STAGES], ready[G::STAGES], empty[G::STAGES];
+  __shared__ StageMeta meta[G::STAGES];
+  __shared__ StageCounts sc[G::STAGES];
+  __shared__ CounterShare cshare[G::STAGES];
 
   Ctl *ctl = Pg->ctl;  // (the on-chip copy is complete after the barrier below)
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u);
   const uint32_t ntiles = ctl->cur_ntiles;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) cshare[s].finished = 0;
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < G::STAGES; ++s) cshare[s].finished = 0;
+    for (int s = 0; s < G::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&aggr[s], 1);
       mbar_init(&ready[s], 1);
@@ -520,13 +520,13 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
     return;
   }
   if (warp >= kLookbackWarp) {
-    lookback_loop<PAY>(P, cur, aggr, ready, meta, warp - kLookbackWarp);
+    lookback_loop<PAY, G::STAGES>(P, cur, aggr, ready, meta, warp - kLookbackWarp);
     return;
   }
   int pend = -1;  // (thread 0) the stage the last bulk stores may still be reading
   for (uint32_t k = 0;; ++k) {
-    const int s = (int)(k % kStages);
-    wait_ready_consumer(&ready[s], (k / kStages) & 1u);
+    const int s = (int)(k % G::STAGES);
+    wait_ready_consumer(&ready[s], (k / G::STAGES) & 1u);
     if (meta[s].kind == KIND_DONE) break;
     emit_tile<C, PAY>(P, k, in_k, in_p, empty, meta, sc, pend);
   }

@@ -43,10 +43,11 @@ constexpr int kLookbackWarps = 2;                 // alternate stages between th
 constexpr int kCounterWarp = kLookbackWarp + kLookbackWarps;  // warps 11-14: counts
 constexpr int kCounterWarps = 4;
 constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps + kCounterWarps);
+// stage ring depth: records 6 (24 KB tiles), keys only TSQ_STAGES (see Geo)
 #ifndef TSQ_STAGES
-#define TSQ_STAGES 6
+#define TSQ_STAGES 4
 #endif
-constexpr int kStages = TSQ_STAGES;               // stage ring depth
+constexpr int kStages = 6;                        // upper bound (barrier arrays)
 constexpr int kAlign = 4;                         // bulk-copy element alignment
 constexpr int kOutPad = 16;                       // alignment slack of a restaged tile
 constexpr uint32_t kDone = 0xffffffffu;
@@ -55,7 +56,21 @@ template <class C, bool PAY>
 struct Geo {
   typedef typename C::U U;
   static constexpr int VN = Vec<U>::N;     // keys per 16-byte vector
-  static constexpr int VPT = 4;            // vectors per thread per tile
+#ifndef TSQ_VPT
+#define TSQ_VPT 6
+#endif
+  // Tile geometry (measured on B200, scripts/variants.py): a tile costs a
+  // fixed share of pipeline work besides its bytes, so keys-only tiles are
+  // 24 KB -- 6 vectors per thread (6144 int32 / 3072 64-bit keys) in a
+  // 4-deep ring, 2 CTAs/SM -- like the 64-bit-key records' 2048-key tiles
+  // (16 KB keys + 8 KB payloads, 4-deep ring).  16 KB int32 tiles ran the
+  // pass 9.5 % slower, 32 KB tiles need a 3-deep ring and lose more;
+  // 64-bit records 5 % slower with the 6-deep ring (1 CTA/SM); 32-bit
+  // records (32 KB stages) are best with 6 (8 % faster than 4).  The
+  // counters' 10-bit lane-scan fields hold a warp slice of up to 1023 keys
+  // (32 * IPT).
+  static constexpr int VPT = PAY ? 4 : TSQ_VPT;
+  static constexpr int STAGES = PAY ? (sizeof(U) == 8 ? 4 : 6) : TSQ_STAGES;
   static constexpr int IPT = VN * VPT;     // keys per thread per tile
   static constexpr int TILE = kConsumers * IPT;
   // a stage holds a tile as loaded and then, restaged in place, its output
@@ -63,7 +78,9 @@ struct Geo {
   static constexpr int SLOT = TILE + kOutPad;
   static constexpr size_t KB = sizeof(U);
   static constexpr size_t STAGE_BYTES = (size_t)SLOT * (KB + (PAY ? 4 : 0));
-  static constexpr size_t SMEM = (size_t)kStages * STAGE_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES;
+  static_assert(STAGES <= kStages, "stage ring deeper than the barrier arrays");
+  static_assert(32 * IPT <= 1023, "counter lane-scan fields are 10 bits");
 };
 
 __device__ __forceinline__ void unpack(const uint4 &v, uint32_t *o) {

@@ -71,8 +71,8 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
   const u64 grid = gridDim.x;
   TileSeg mine;  // lane j: the tile of iteration (it & ~31) + j
   for (uint32_t it = 0;; ++it) {
-    const int s = (int)(it % kStages);
-    const uint32_t j = it / kStages;
+    const int s = (int)(it % G::STAGES);
+    const uint32_t j = it / G::STAGES;
     const u64 t64 = blockIdx.x + (u64)it * grid;
     if ((it & 31u) == 0) {
       const u64 tl = blockIdx.x + (u64)(it + lane) * grid;
@@ -86,9 +86,9 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
       const int markers = kLookbackWarps;
       for (int e = 0; e < markers; ++e) {
         const uint32_t ie = it + (uint32_t)e;
-        const int se = (int)(ie % kStages);
-        if (e > 0 && ie >= (uint32_t)kStages)
-          wait_empty_producer(&empty[se], (ie / kStages - 1) & 1u);
+        const int se = (int)(ie % G::STAGES);
+        if (e > 0 && ie >= (uint32_t)G::STAGES)
+          wait_empty_producer(&empty[se], (ie / G::STAGES - 1) & 1u);
         if (lane == 0) {
           meta[se].kind = KIND_DONE;
           meta[se].k = (uint32_t)e;
@@ -219,7 +219,7 @@ __device__ __forceinline__ u64 lookback_window(u64 *lb, long long base, long lon
 // atomic on the segment's fill word (the first tile's descriptor slot; the
 // records' == payload slots on the segment's eq_fill).  Either way the
 // counters never wait on a global round trip.
-template <bool PAY>
+template <bool PAY, int NS>
 __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *aggr, u64 *ready,
                                               StageMeta *meta, int lw) {
   const int lane = threadIdx.x & 31;
@@ -228,8 +228,8 @@ __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *agg
   const uint32_t level = P->ctl->level;
   (void)level;
   for (uint32_t it = (uint32_t)lw;; it += kLookbackWarps) {
-    const int s = (int)(it % kStages);
-    wait_aggr_lookback(&aggr[s], (it / kStages) & 1u);
+    const int s = (int)(it % NS);
+    wait_aggr_lookback(&aggr[s], (it / NS) & 1u);
     StageMeta &m = meta[s];
     if (m.kind == KIND_DONE) {
       // the first marker goes on to the consumers; later ones only stop

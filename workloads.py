@@ -71,6 +71,9 @@ def generate(family: str, n: int, seed: int = SEED):
     if family == "records":
         keys = rng.integers(0, 2**20, n, dtype=np.uint64)
         return keys, np.arange(n, dtype=np.uint32)
+    if family == "records_u32":  # (not a BASELINE config: 32-bit-key records, dev sweeps)
+        keys = rng.integers(0, 2**20, n, dtype=np.uint64).astype(np.uint32)
+        return keys, np.arange(n, dtype=np.uint32)
     raise KeyError(f"unknown family {family!r}; valid: {', '.join(FAMILIES)}")
 
 
