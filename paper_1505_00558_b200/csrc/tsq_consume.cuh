@@ -357,11 +357,16 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   const uint32_t level = P->ctl->level;
   (void)level;
   if (m.kind != KIND_PARTITION) {
-    // verified by the counters: nothing to write.  The stage the last
-    // partition tile's bulk stores were reading is released here too --
-    // otherwise a run of verification tiles after a partition tile would
-    // leave it held until the next partition tile, and the producer,
-    // wrapping around the ring onto it, would stall the pipeline for good.
+    // verified by the counters: nothing to write.  Every consumer warp must
+    // have read this stage's meta before the stage goes back to the
+    // producer (which rewrites it for a later tile): a warp that lagged
+    // would otherwise take the next tile's kind for this one and leave the
+    // consumers' named barriers out of step.  The stage the last partition
+    // tile's bulk stores were reading is released here too -- otherwise a
+    // run of verification tiles after a partition tile would leave it held
+    // until the next partition tile, and the producer, wrapping around the
+    // ring onto it, would stall the pipeline for good.
+    named_sync(1, kConsumers);
     if (tid == 0) {
       if (pend >= 0) {
         bulk_wait_read0();

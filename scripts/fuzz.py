@@ -17,6 +17,8 @@ import paper_1505_00558_b200 as T
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+only = int(sys.argv[3]) if len(sys.argv) > 3 else -1          # replay one case
+host_levels = os.environ.get("TSQ_FUZZ_HOST_LEVELS") == "1"
 rng = np.random.default_rng(seed)
 DT = [np.int32, np.uint32, np.float32, np.int64, np.uint64, np.float64]
 
@@ -69,10 +71,15 @@ for c in range(cases):
                         rng.integers(70000, 3_000_000)]))
     x, kind = keys_of(dt, n)
     thr = int(rng.choice([0, 0, 0, 1, 3, 16, 4096, 8192, 16384]))
+    if os.environ.get("TSQ_FUZZ_TINY") == "1":  # stress: the partition machine down to tiny segments
+        thr = int(rng.choice([1, 2, 3]))
     rep = bool(rng.integers(0, 2))
     pay = bool(rng.integers(0, 3) == 0)
     s = T.Sorter(seed=int(rng.integers(1, 1 << 30)),
-                 gpu=T.GpuConfig(small_threshold=thr, reproducible=rep))
+                 gpu=T.GpuConfig(small_threshold=thr, reproducible=rep, host_levels=host_levels,
+                                 fast_paths=os.environ.get("TSQ_FUZZ_NOFP") != "1"))
+    if only >= 0 and c != only:
+        continue
     d = torch.from_numpy(x.copy()).cuda()
     print(f"case {c}: dtype={np.dtype(dt).name} n={n} kind={kind} thr={thr} rep={rep} pay={pay}",
           flush=True)

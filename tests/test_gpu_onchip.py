@@ -165,3 +165,37 @@ def test_verification_tiles_after_partition_tiles(cuda_ok):
             d = torch.from_numpy(x.copy()).cuda()
             T.Sorter(seed=3, gpu=T.GpuConfig(small_threshold=1)).sort(d)
             assert d.cpu().numpy().tobytes() == np.sort(x).tobytes()
+
+
+def test_tiny_cut_stress_verification_tiles(cuda_ok):
+    """Regression (race): with cuts of 1-3 keys the partition pass handles
+    thousands of 2-3-key segments, many of them verification tiles
+    (sorted / reversed fast paths).  Their stage must not go back to the
+    producer before every consumer warp has read its meta -- a lagging warp
+    used to pick up the next tile's kind and stall the pipeline (~1 in 300
+    such sorts).  Keys bit-exact, records consistent."""
+    rng = np.random.default_rng(2024)
+    for trial in range(60):
+        dt = [np.int32, np.uint64, np.float32, np.int64][trial % 4]
+        n = int(rng.integers(2000, 60000))
+        base = rng.integers(0, 1 << 20, n).astype(dt)
+        shape = trial % 3
+        if shape == 1:
+            base = np.sort(base)
+            k = max(1, n // 100)
+            a, b = rng.integers(0, n, k), rng.integers(0, n, k)
+            base[a], base[b] = base[b], base[a]
+        elif shape == 2:
+            i = np.arange(n)
+            base = np.minimum(i, n - 1 - i).astype(dt)
+        g = T.GpuConfig(small_threshold=int(rng.integers(1, 4)), reproducible=bool(trial & 4))
+        d = torch.from_numpy(base.copy()).cuda()
+        if trial % 5 == 0:
+            from conftest import assert_records_consistent
+            p = torch.arange(n, dtype=torch.int64).to(torch.uint32).cuda()
+            T.Sorter(seed=trial + 1, gpu=g).sort(T.Records(d, p))
+            assert_records_consistent(base, d.cpu().numpy(), p.cpu().numpy().astype(np.int64),
+                                      np.sort(base))
+        else:
+            T.Sorter(seed=trial + 1, gpu=g).sort(d)
+            assert d.cpu().numpy().tobytes() == np.sort(base).tobytes()
