@@ -125,7 +125,7 @@ def reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n_sample = 1 << 24
+    n_sample = 1 << args.sample_log2
     vals = []
     for i in range(args.warmup + args.steps):
         v, _ = cpu_baseline(n_sample, threads, args.family)
@@ -137,11 +137,12 @@ def reference_arm(args, rank: int, world: int):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": n_sample / value * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.family} int32 n=2^26 (bounded sample n=2^24 per step)",
+        "config": {"workload": f"{args.family} int32 n=2^26 (bounded sample "
+                                f"n=2^{args.sample_log2} per step)",
                    "n": args.n, "sample_n": n_sample},
         "cpu_baseline": {"value": value, "unit": "keys/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.family} int32 n=2^24 per step, oracle/ C "
-                                   f"restatement with {threads} OpenMP threads"},
+                         "sample": f"{args.family} int32 n=2^{args.sample_log2} per step, "
+                                   f"oracle/ C restatement with {threads} OpenMP threads"},
         "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -349,6 +350,8 @@ def main():
     ap.add_argument("--n", type=int, default=1 << 26)
     ap.add_argument("--families", action="store_true", help="add a per-family table")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sample-log2", type=int, default=24,
+                    help="reference arm: keys per timed CPU sample (2^k)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
