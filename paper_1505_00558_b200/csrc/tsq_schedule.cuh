@@ -51,7 +51,8 @@ __device__ __forceinline__ void append_small(const Params *P, long long begin, l
 template <class C, bool PAY>
 __device__ __forceinline__ uint32_t tiles_of(long long begin, long long end) {
   const long long T = Geo<C, PAY>::TILE;
-  return (uint32_t)((end - 1) / T - begin / T + 1);
+  // segment-anchored tile grid (producer_loop, tsq_partition.cuh)
+  return (uint32_t)(((end - 1) - (begin & ~(long long)(kAlign - 1))) / T + 1);
 }
 
 __device__ __forceinline__ uint32_t chunks_of(uint32_t kind, long long len, uint32_t buf) {
