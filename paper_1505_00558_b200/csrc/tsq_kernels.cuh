@@ -47,7 +47,7 @@ constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps + kCounterWar
 #ifndef TSQ_STAGES
 #define TSQ_STAGES 4
 #endif
-constexpr int kStages = 6;                        // upper bound (barrier arrays)
+constexpr int kStages = 8;                        // upper bound on any ring depth
 constexpr int kAlign = 4;                         // bulk-copy element alignment
 constexpr int kOutPad = 16;                       // alignment slack of a restaged tile
 constexpr uint32_t kDone = 0xffffffffu;
