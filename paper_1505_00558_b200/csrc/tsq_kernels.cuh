@@ -7,7 +7,7 @@
 //                      multi-block three-way partition (the stage that
 //                      _run_machine performs, core.py:198-984).  Persistent,
 //                      warp-specialised (tsq_partition.cuh): a producer warp
-//                      streams tiles into a 6-deep shared-memory ring with
+//                      streams 24 KB tiles into a 4- or 6-deep shared-memory ring with
 //                      cp.async.bulk (TMA engine) + mbarriers; counter warps
 //                      count each consumer thread's < / > keys; look-back
 //                      warps turn tile counts into output offsets; consumer

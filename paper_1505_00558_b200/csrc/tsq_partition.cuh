@@ -8,7 +8,7 @@
 //
 // Persistent CTAs (2 per SM), warp-specialised (480 threads):
 //   warp 8       producer: deals tiles round-robin, resolves their segments
-//                32 at a time, streams each into a 6-deep shared-memory ring
+//                32 at a time, streams each into a 4- or 6-deep shared-memory ring (Geo)
 //                with cp.async.bulk (TMA engine) completing on the stage's
 //                mbarrier; a DONE marker ends the ring
 //   warps 11-14  counters (tsq_consume.cuh): per consumer thread the (<, >)
