@@ -39,7 +39,10 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;   // 256
 constexpr int kProducerWarp = kConsumerWarps;     // warp 8: tile claims + bulk loads
 constexpr int kLookbackWarp = kConsumerWarps + 1; // warps 9, 10: decoupled look-back
-constexpr int kLookbackWarps = 2;                 // alternate stages between them
+#ifndef TSQ_LB_WARPS
+#define TSQ_LB_WARPS 2
+#endif
+constexpr int kLookbackWarps = TSQ_LB_WARPS;      // alternate stages between them
 constexpr int kCounterWarp = kLookbackWarp + kLookbackWarps;  // warps 11-14: counts
 constexpr int kCounterWarps = 4;
 constexpr int kPartThreads = kConsumers + 32 * (1 + kLookbackWarps + kCounterWarps);

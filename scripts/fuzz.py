@@ -69,6 +69,8 @@ for c in range(cases):
     dt = DT[rng.integers(0, len(DT))]
     n = int(rng.choice([rng.integers(2, 5000), rng.integers(5000, 70000),
                         rng.integers(70000, 3_000_000)]))
+    if os.environ.get("TSQ_FUZZ_BIG") == "1":  # large inputs: 2^22 .. 2^25 keys
+        n = int(rng.integers(1 << 22, 1 << 25))
     x, kind = keys_of(dt, n)
     thr = int(rng.choice([0, 0, 0, 1, 3, 16, 4096, 8192, 16384]))
     if os.environ.get("TSQ_FUZZ_TINY") == "1":  # stress: the partition machine down to tiny segments
