@@ -42,18 +42,47 @@
 extern "C" {
 #endif
 
-#define TSQ_ABI_VERSION 1
+#define TSQ_ABI_VERSION 2
 
 typedef enum {
   TSQ_OK = 0,
   TSQ_ERR_ALLOC = 1,              /* -> TempAllocationError (core.py:46-47) */
   TSQ_ERR_UNSUPPORTED_DTYPE = 2,  /* -> TypeError */
   TSQ_ERR_CUDA = 3,               /* -> RuntimeError */
-  TSQ_ERR_DEPTH_EXCEEDED = 4,     /* depth guard tripped (no O(n^2) fallback) */
+  TSQ_ERR_DEPTH_EXCEEDED = 4,     /* level limit reached (cannot happen: beyond the depth
+                                   * guard segments split at their key-bound midpoint) */
   TSQ_ERR_INVALID = 5,            /* -> ValueError (bad sizes / pointers) */
   TSQ_ERR_BUSY = 6,               /* -> RuntimeError("not reentrant") */
-  TSQ_ERR_CAPACITY = 7            /* internal queue overflow */
+  TSQ_ERR_CAPACITY = 7            /* internal queue overflow (cannot happen: the queues
+                                   * are drained before they could overflow) */
 } tsq_status;
+
+/* One stage of a host-driven level, reported to the on_level callback (the
+ * stage_hook(a, b, new_l, new_r, pivot) / trace STAGE_END contract,
+ * core.py:1705-1710): inclusive bounds a..b, keys[a..new_l] < pivot,
+ * keys[new_l+1..new_r-1] == pivot, keys[new_r..b] > pivot. */
+typedef enum {
+  TSQ_STAGE_PARTITION = 0,        /* three-way partition pass (_run_machine) */
+  TSQ_STAGE_SORTED = 1,           /* verified sorted, bypassed (_sorted_handler) */
+  TSQ_STAGE_REVERSED = 2,         /* verified reversed, mirrored (_reversed_handler) */
+  TSQ_STAGE_HANDLER_FALLBACK = 3  /* verification failed: partitioned next level;
+                                   * new_l = the handler tried (TSQ_STAGE_SORTED or
+                                   * TSQ_STAGE_REVERSED), new_r unset */
+} tsq_stage_kind;
+
+typedef struct {
+  int64_t a, b, new_l, new_r;
+  uint64_t pivot;                 /* raw bits of a key of key_t */
+  int32_t kind;                   /* tsq_stage_kind */
+  int32_t depth;                  /* recursion depth of the stage (root = 1) */
+} tsq_stage_record;
+
+/* Called after every host-driven level once the caller's keys/payload hold
+ * each listed segment's post-stage contents (in stage-export mode the sort
+ * runs in an internal copy and the caller's buffers are a view of the
+ * recursion; they receive the sorted result at the end). */
+typedef void (*tsq_level_fn)(void *user, int32_t level, const tsq_stage_record *records,
+                             uint32_t count);
 
 typedef enum {
   TSQ_NONE = 0,
@@ -71,7 +100,9 @@ typedef struct {
   double dran;             /* MitigationRng.dran in [0.5,1.5) (pivot.py:45-49); 0 -> 1.0 */
   int32_t mitigation;      /* jitter sample positions by dran (config.py:24) */
   int32_t fast_paths;      /* sorted/reversed verify-and-bypass (core.py:1678-1698); default 1 */
-  int32_t max_depth;       /* depth guard; default 96 */
+  int32_t max_depth;       /* depth guard: deeper segments are split at the midpoint of
+                            * their key bounds (no sampling), which ends the recursion
+                            * within key-bits more levels; 0 = max(24, 2 log2 n) */
   int32_t host_levels;     /* 1 = drive levels from the host (debug/per-level stats) */
   int32_t small_threshold; /* segments <= this go on chip (1..16384); 0 = the default:
                             * 4-byte keys 16384 (8192 up to 2^21 keys; records 8192),
@@ -79,7 +110,10 @@ typedef struct {
                             * capacity */
   int32_t reproducible;    /* 1 = run-to-run identical layout (decoupled look-back);
                             * 0 = tiles reserve output ranges with one atomic (faster) */
-  int64_t reserved[3];
+  int32_t stage_export;    /* 1 = host-driven levels with on_level called per level */
+  tsq_level_fn on_level;   /* stage_export callback (may be NULL) */
+  void *on_level_user;
+  int64_t reserved[1];
 } tsq_params;
 
 /* Counters of one call (the SortStats analogue, stats.py:33-70). */
@@ -102,6 +136,8 @@ typedef struct {
   uint64_t error_flags;
   uint64_t writes_caller;      /* element writes into the caller's array */
   uint64_t writes_workspace;   /* element writes into the workspace */
+  uint64_t bisected;           /* segments split at their key-bound midpoint (depth guard) */
+  uint64_t flushes;            /* mid-recursion drains of the on-chip / run queues */
   float ms_levels;             /* device time of the level loop (events) */
   float ms_total;              /* device time of the whole sort (events) */
 } tsq_stats;
@@ -124,9 +160,17 @@ tsq_status tsq_workspace_free(tsq_workspace *ws);
 /* elements the workspace currently holds capacity for; allocation count */
 size_t tsq_workspace_capacity(const tsq_workspace *ws);
 uint64_t tsq_workspace_alloc_count(const tsq_workspace *ws);
+/* Outcome of the last sort on this workspace: waits for it (on `stream`)
+ * and maps its device error flags to a status (TSQ_OK when it finished). */
+tsq_status tsq_workspace_last_status(tsq_workspace *ws, void *stream);
 
 /* Sort keys[0..n) ascending in place; payload (nullable, TSQ_U32) moves with
- * its key (records compared by key only).  stats may be NULL (no sync). */
+ * its key (records compared by key only).  keys must be aligned to its
+ * element size and payload to 4 bytes (else TSQ_ERR_INVALID); buffers that
+ * are not 16-byte aligned (views with a storage offset) are sorted through
+ * an aligned workspace copy.  stats may be NULL: the call then returns
+ * without synchronising, and tsq_workspace_last_status reports the
+ * outcome. */
 tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t,
                     tsq_dtype payload_t, const tsq_params *params,
                     tsq_workspace *ws, void *stream, tsq_stats *stats);

@@ -10,9 +10,10 @@ raises if the library or the device is missing (no CPU fallback).
 """
 
 from .config import DEFAULT_CONFIG, DEFAULT_GPU_CONFIG, GpuConfig, SortConfig
-from .core import (DepthExceededError, DeviceTempStore, Records, Sorter,
-                   TempAllocationError, free_temp_storage, key_cmp, sort, sort_many,
-                   sort_with_stats)
+from .core import (DepthExceededError, DeviceTempStore, PartitionFrame, Records, Sorter,
+                   TempAllocationError, TempStore, free_temp_storage, key_cmp, sort,
+                   sort_many, sort_with_stats)
+from .instrument import TraceSink
 from .bigelem import Permutation, apply_permutation, sort_indirect
 from .pivot import MitigationRng, rng_next
 from .stats import SortStats
@@ -38,7 +39,8 @@ def get_algorithm(name: str):
 
 __all__ = [
     "DEFAULT_CONFIG", "DEFAULT_GPU_CONFIG", "DepthExceededError", "DeviceTempStore",
-    "GpuConfig", "MitigationRng", "Permutation", "REGISTRY", "Records", "SortConfig", "SortStats",
-    "Sorter", "TempAllocationError", "apply_permutation", "free_temp_storage", "get_algorithm",
-    "key_cmp", "rng_next", "sort", "sort_indirect", "sort_many", "sort_with_stats",
+    "GpuConfig", "MitigationRng", "PartitionFrame", "Permutation", "REGISTRY", "Records",
+    "SortConfig", "SortStats", "Sorter", "TempAllocationError", "TempStore", "TraceSink",
+    "apply_permutation", "free_temp_storage", "get_algorithm", "key_cmp", "rng_next", "sort",
+    "sort_indirect", "sort_many", "sort_with_stats",
 ]

@@ -23,14 +23,31 @@ EXPORTED_SYMBOLS = (
     "tsq_workspace_bytes", "tsq_workspace_reserve", "tsq_workspace_free",
     "tsq_workspace_capacity", "tsq_workspace_alloc_count", "tsq_sort",
     "tsq_partition_segment", "tsq_select_pivot", "tsq_level_trace", "tsq_apply_permutation",
+    "tsq_workspace_last_status",
 )
+
+# tsq_stage_kind (include/tsq.h)
+TSQ_STAGE_PARTITION, TSQ_STAGE_SORTED, TSQ_STAGE_REVERSED, TSQ_STAGE_HANDLER_FALLBACK = range(4)
+
+
+class TsqStageRecord(ctypes.Structure):
+    _fields_ = [("a", ctypes.c_int64), ("b", ctypes.c_int64), ("new_l", ctypes.c_int64),
+                ("new_r", ctypes.c_int64), ("pivot", ctypes.c_uint64), ("kind", ctypes.c_int32),
+                ("depth", ctypes.c_int32)]
+
+
+# void (*)(void *user, int32_t level, const tsq_stage_record *records, uint32_t count)
+LEVEL_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int32,
+                            ctypes.POINTER(TsqStageRecord), ctypes.c_uint32)
 
 
 class TsqParams(ctypes.Structure):
     _fields_ = [("dran", ctypes.c_double), ("mitigation", ctypes.c_int32),
                 ("fast_paths", ctypes.c_int32), ("max_depth", ctypes.c_int32),
                 ("host_levels", ctypes.c_int32), ("small_threshold", ctypes.c_int32),
-                ("reproducible", ctypes.c_int32), ("reserved", ctypes.c_int64 * 3)]
+                ("reproducible", ctypes.c_int32), ("stage_export", ctypes.c_int32),
+                ("on_level", LEVEL_FN), ("on_level_user", ctypes.c_void_p),
+                ("reserved", ctypes.c_int64 * 1)]
 
 
 class TsqStats(ctypes.Structure):
@@ -38,7 +55,7 @@ class TsqStats(ctypes.Structure):
         "n", "stages", "levels", "max_depth", "small_segments", "eq_runs", "eq_elements",
         "sorted_bypass", "reversed_bypass", "verify_fallbacks", "partitioned_elements",
         "bytes_partition", "bytes_small", "bytes_retire", "temp_high_water", "error_flags",
-        "writes_caller", "writes_workspace")] + \
+        "writes_caller", "writes_workspace", "bisected", "flushes")] + \
         [("ms_levels", ctypes.c_float), ("ms_total", ctypes.c_float)]
 
     def as_dict(self) -> dict:
@@ -105,6 +122,8 @@ def lib():
         L.tsq_level_trace.restype = i32
         L.tsq_apply_permutation.argtypes = [vp, vp, sz, sz, vp, vp]
         L.tsq_apply_permutation.restype = i32
+        L.tsq_workspace_last_status.argtypes = [vp, vp]
+        L.tsq_workspace_last_status.restype = i32
         _lib = L
     return _lib
 

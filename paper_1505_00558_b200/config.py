@@ -49,7 +49,11 @@ class GpuConfig:
     fast_paths   verify-and-bypass segments whose samples look sorted or
                  reversed (the _sorted_handler / _reversed_handler role,
                  core.py:991-1556); results are identical either way.
-    max_depth    depth guard; exceeding it raises instead of degrading.
+    max_depth    depth guard: segments deeper than this are split at the
+                 midpoint of their key bounds instead of a sampled pivot,
+                 which ends every segment within key-bits more levels (the
+                 reference's _range always finishes, core.py:1643-1728);
+                 0 = max(24, 2 * ceil(log2 n)).
     small_threshold  segments of at most this many keys finish in the on-chip
                  sort; 0 = the measured default (4-byte keys 16384 -- 8192 up
                  to 2^21 keys --, records and 8-byte keys 8192); values above
@@ -69,7 +73,7 @@ class GpuConfig:
     """
 
     fast_paths: bool = True
-    max_depth: int = 96
+    max_depth: int = 0
     host_levels: bool = False
     small_threshold: int = 0
     reproducible: bool = False
@@ -77,8 +81,8 @@ class GpuConfig:
     def __post_init__(self):
         if not (self.small_threshold == 0 or 1 <= self.small_threshold <= 16384):
             raise ValueError("small_threshold must be 0 (auto) or in [1, 16384]")
-        if not 8 <= self.max_depth <= 190:
-            raise ValueError("max_depth must be in [8, 190]")
+        if not (self.max_depth == 0 or 2 <= self.max_depth <= 190):
+            raise ValueError("max_depth must be 0 (auto) or in [2, 190]")
 
 
 DEFAULT_GPU_CONFIG = GpuConfig()

@@ -35,12 +35,13 @@ import numpy as np
 
 from . import _native as N
 from .config import DEFAULT_CONFIG, DEFAULT_GPU_CONFIG, GpuConfig, SortConfig
+from .instrument import HANDLER_ENTER, HANDLER_FALLBACK, STAGE_END, STATE_ENTER
 from .pivot import MitigationRng
 from .stats import SortStats
 
 __all__ = ["TempAllocationError", "DepthExceededError", "Records", "key_cmp",
-           "DeviceTempStore", "Sorter", "sort", "sort_with_stats", "sort_many",
-           "free_temp_storage", "default_sorter"]
+           "DeviceTempStore", "TempStore", "PartitionFrame", "Sorter", "sort",
+           "sort_with_stats", "sort_many", "free_temp_storage", "default_sorter"]
 
 
 class TempAllocationError(MemoryError):
@@ -48,7 +49,9 @@ class TempAllocationError(MemoryError):
 
 
 class DepthExceededError(RuntimeError):
-    """The device recursion exceeded GpuConfig.max_depth."""
+    """The device level loop hit its hard limit.  Cannot happen in practice:
+    beyond GpuConfig.max_depth segments are split at the midpoint of their
+    key bounds, which ends every segment within key-bits more levels."""
 
 
 def key_cmp(x, y) -> int:
@@ -105,38 +108,78 @@ def _raise_status(st: int, what: str):
 class DeviceTempStore:
     """Retained device workspace (TempStore, core.py:81-104).
 
+    One workspace per CUDA device the sorter has sorted on (a tensor on
+    cuda:1 sorts with cuda:1's workspace, whatever the current device).
     ``capacity`` is the element count of the largest sort served since the
     last release; ``alloc_count`` counts device allocations.
     """
 
     def __init__(self, device: int | None = None):
-        self.device = device
-        self._ws = None
+        self.device = device   # default device: host containers are staged here
+        self._ws = {}
 
-    def workspace(self) -> N.Workspace:
-        if self._ws is None:
+    def workspace(self, device: int | None = None) -> N.Workspace:
+        if device is None:
+            device = self.device
+        if device is None:
             torch = _torch()
             if not torch.cuda.is_available():
                 raise RuntimeError("no CUDA device: the B200 sort has no CPU fallback")
-            dev = torch.cuda.current_device() if self.device is None else self.device
-            self.device = dev
-            self._ws = N.Workspace(dev)
-        return self._ws
+            device = torch.cuda.current_device()
+        if self.device is None:
+            self.device = device
+        ws = self._ws.get(device)
+        if ws is None:
+            ws = self._ws[device] = N.Workspace(device)
+        return ws
 
     @property
     def capacity(self) -> int:
-        return self._ws.capacity if self._ws is not None else 0
+        return max((w.capacity for w in self._ws.values()), default=0)
 
     @property
     def alloc_count(self) -> int:
-        return self._ws.alloc_count if self._ws is not None else 0
+        return sum(w.alloc_count for w in self._ws.values())
 
-    def ensure(self, n: int, key_dt: int = N.TSQ_I32, pay_dt: int = N.TSQ_NONE) -> None:
-        _raise_status(self.workspace().reserve(n, key_dt, pay_dt), "workspace reserve")
+    def ensure(self, n: int, key_dt: int = N.TSQ_I32, pay_dt: int = N.TSQ_NONE,
+               device: int | None = None) -> None:
+        _raise_status(self.workspace(device).reserve(n, key_dt, pay_dt), "workspace reserve")
 
     def release(self) -> None:
-        if self._ws is not None:
-            _raise_status(self._ws.free(), "workspace free")
+        for w in self._ws.values():
+            _raise_status(w.free(), "workspace free")
+
+
+# The reference's names for the retained buffer and the stage frame
+# (/root/reference/pkg/src/tsqsort/__init__.py:16-18).  TempStore is the
+# device workspace here.  PartitionFrame describes one stage -- the
+# (a, b, new_l, new_r, pivot) a stage_hook receives -- with the reference's
+# field names; the device recursion has no per-stage frame object of its
+# own (core.py:58-78).
+TempStore = DeviceTempStore
+
+
+class PartitionFrame:
+    """Index set and pivot of one stage (core.py:58-78): ``a..b`` inclusive,
+    after the stage ``[a..new_l] < pivot``, ``(new_l, new_r) == pivot``,
+    ``[new_r..b] > pivot``."""
+
+    __slots__ = ("a", "b", "mid", "pi", "pivot", "new_l", "new_r", "depth", "kind")
+
+    def __init__(self, a=0, b=-1, pi=None, pivot=None):
+        self.a = a
+        self.b = b
+        self.mid = (a + b) >> 1
+        self.pi = self.mid if pi is None else pi
+        self.pivot = pivot
+        self.new_l = a - 1
+        self.new_r = b + 1
+        self.depth = 0
+        self.kind = "partition"
+
+    def __repr__(self):
+        return (f"PartitionFrame(a={self.a}, b={self.b}, new_l={self.new_l}, "
+                f"new_r={self.new_r}, pivot={self.pivot!r}, kind={self.kind!r})")
 
 
 class _Job:
@@ -370,8 +413,8 @@ class Sorter:
             self._bind(job, kt, pt, codes)
             inner = job.finish
 
-            def finish_records():
-                inner()
+            def finish_records(final=True):
+                inner(final)
                 perm = pay
                 ar[:] = [values[i] for i in perm.tolist()]
 
@@ -382,8 +425,8 @@ class Sorter:
         self._bind(job, kt, None, codes)
         inner = job.finish
 
-        def finish_list():
-            inner()
+        def finish_list(final=True):
+            inner(final)
             ar[:] = arr.tolist()
 
         job.finish = finish_list
@@ -399,7 +442,7 @@ class Sorter:
         job.key_dt = codes[keys.dtype]
         job.pay_dt = N.TSQ_U32 if payload is not None else N.TSQ_NONE
         if job.n <= 1:
-            job.finish = lambda: None
+            job.finish = lambda final=True: None
             return
         outs = []
         devs = []
@@ -422,12 +465,17 @@ class Sorter:
                 outs.append((t, d))
         job.keys, job.payload = devs
 
-        def finish():
+        if payload is not None and keys.is_cuda and payload.is_cuda and \
+                keys.device != payload.device:
+            raise ValueError("keys and payload must be on the same device")
+
+        def finish(final=True):
+            # final=False: a stage-export refresh of the host container
             if not outs:
                 return
             for dst, src in outs:
                 dst.copy_(src, non_blocking=not dst.is_cuda)
-                if not dst.is_cuda:
+                if final and not dst.is_cuda:
                     job.d2h_bytes += dst.numel() * dst.element_size()
             torch.cuda.current_stream(src.device).synchronize()
 
@@ -439,9 +487,10 @@ class Sorter:
         if job.n <= 1:
             return stats
         torch = _torch()
+        dev = job.keys.device.index
         # allocation precedes any mutation (core.py:1599): the array stays
         # untouched if this raises
-        self.temp.ensure(job.n, job.key_dt, job.pay_dt)
+        self.temp.ensure(job.n, job.key_dt, job.pay_dt, dev)
         self.rng.next()
         p = N.TsqParams()
         p.dran = self.rng.dran
@@ -450,24 +499,87 @@ class Sorter:
         p.max_depth = self.gpu.max_depth
         p.small_threshold = self.gpu.small_threshold
         p.reproducible = 1 if self.gpu.reproducible else 0
-        p.host_levels = 1 if (self.gpu.host_levels or self.stage_hook is not None) else 0
+        p.host_levels = 1 if self.gpu.host_levels else 0
+        hook, trace = self.stage_hook, self.trace
+        errors = []
+        if hook is not None or trace is not None:
+            # stage export: after every device level the caller's array holds
+            # each stage's post-stage contents, then hook(a, b, new_l, new_r,
+            # pivot) runs per stage and the trace gets its events
+            # (core.py:1676-1710)
+            decode = _pivot_decoder(job.keys.dtype)
+
+            def on_level(_user, level, recs, count):
+                if errors:
+                    return
+                try:
+                    job.finish(False)
+                    for i in range(count):
+                        _emit_stage(recs[i], decode, hook, trace)
+                except BaseException as exc:  # re-raised after the call
+                    errors.append(exc)
+
+            cb = N.LEVEL_FN(on_level)
+            p.stage_export = 1
+            p.on_level = cb
         ts = N.TsqStats()
-        dev = job.keys.device
         stream = torch.cuda.current_stream(dev).cuda_stream
-        ws = self.temp.workspace()
+        ws = self.temp.workspace(dev)
         st = N.lib().tsq_sort(
             ctypes.c_void_p(job.keys.data_ptr()),
             ctypes.c_void_p(job.payload.data_ptr()) if job.payload is not None else None,
             job.n, job.key_dt, job.pay_dt, ctypes.byref(p), ws.handle,
             ctypes.c_void_p(stream), ctypes.byref(ts))
+        if errors:
+            raise errors[0]
         _raise_status(st, "tsq_sort")
-        if p.host_levels:
+        if p.host_levels or p.stage_export:
             self.last_level_trace = ws.level_trace()
-            if self.stage_hook is not None:
-                for i, lv in enumerate(self.last_level_trace):
-                    self.stage_hook(i, lv)
         job.finish()
+        if trace is not None:
+            trace.emit(STAGE_END, 0, job.n - 1, "root")
         return _to_stats(ts, job)
+
+
+
+
+def _pivot_decoder(dtype):
+    """Raw bits of a key of ``dtype`` -> the Python value."""
+    torch = _torch()
+    np_dt = {torch.int32: np.int32, torch.uint32: np.uint32, torch.int64: np.int64,
+             torch.uint64: np.uint64, torch.float32: np.float32,
+             torch.float64: np.float64}[dtype]
+    bits_dt = np.uint32 if np.dtype(np_dt).itemsize == 4 else np.uint64
+
+    def decode(bits: int):
+        return np.asarray([bits], dtype=np.uint64).astype(bits_dt).view(np_dt)[0].item()
+
+    return decode
+
+
+def _emit_stage(rec, decode, hook, trace) -> None:
+    """One device stage record -> stage_hook call and trace events, in the
+    order the reference's _range emits them (core.py:1676-1710)."""
+    a, b = int(rec.a), int(rec.b)
+    kind = int(rec.kind)
+    if kind == N.TSQ_STAGE_HANDLER_FALLBACK:
+        if trace is not None:
+            name = "sorted" if int(rec.new_l) == N.TSQ_STAGE_SORTED else "reversed"
+            trace.emit(HANDLER_ENTER, name, a, b)
+            trace.emit(HANDLER_FALLBACK, name, "prescan")
+        return
+    pivot = decode(int(rec.pivot))
+    new_l, new_r = int(rec.new_l), int(rec.new_r)
+    if trace is not None:
+        if kind == N.TSQ_STAGE_PARTITION:
+            trace.emit(STATE_ENTER, "prescan", a, b)
+        else:
+            trace.emit(HANDLER_ENTER, "sorted" if kind == N.TSQ_STAGE_SORTED else "reversed",
+                       a, b)
+    if hook is not None:
+        hook(a, b, new_l, new_r, pivot)
+    if trace is not None:
+        trace.emit(STAGE_END, a, b, new_l, new_r)
 
 
 def _rows_payload(ar) -> bool:

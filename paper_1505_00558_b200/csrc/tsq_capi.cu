@@ -4,6 +4,7 @@
 // trip: a conditional WHILE node re-launches the level kernel until the
 // device queue is empty), and the extern "C" entry points of include/tsq.h.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -19,7 +20,7 @@ using namespace tsq;
 namespace {
 
 struct KernelSet {
-  const void *init, *part, *sched, *retire, *selp;
+  const void *init, *part, *sched, *retire, *selp, *exportk;
   int key_bytes, tile;
   size_t part_smem, sched_smem;
   // on-chip sort classes: 256 / 512 threads (tsq_small.cuh)
@@ -62,6 +63,7 @@ KernelSet make_set() {
   s.raw_order = C::kRawOrder;
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
+  s.exportk = reinterpret_cast<const void *>(&export_level_kernel<C, PAY>);
   s.key_bytes = (int)sizeof(U);
   s.tile = Geo<C, PAY>::TILE;
   s.part_smem = Geo<C, PAY>::SMEM;
@@ -118,11 +120,14 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   size_t keys_alt, pay_alt, side_pay, segs[2], tilemap[2], lookback[2], sq[kSmallClasses], runs,
       chunkmap;
+  size_t stage_keys, stage_pay;  // aligned copies of the caller's buffers (staged sorts)
+  size_t stage_out;              // per-segment stage records (stage-export mode)
   size_t total;
   uint32_t seg_cap, tile_cap, run_cap, chunk_cap, sq_cap[kSmallClasses];
 };
 
-Layout make_layout(size_t n, int kt, int pt, int small_t = 0) {
+Layout make_layout(size_t n, int kt, int pt, int small_t = 0, bool staged = false,
+                   bool export_records = false) {
   if (small_t <= 0) small_t = default_small_t(kt, pt, n);
   Layout L;
   memset(&L, 0, sizeof(L));
@@ -134,6 +139,12 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = 0) {
   L.run_cap = 8u * L.seg_cap + 64u;
   L.sq_cap[0] = 2u * L.run_cap;
   L.sq_cap[1] = (uint32_t)(n / (size_t)(kSmallT + 1) + 2);
+  if (getenv("TSQ_DEBUG_MIN_QUEUES")) {
+    // test knob: the smallest queues the flush rule allows, so the level
+    // loop drains them every level or two (exercises the drain rounds)
+    L.run_cap = L.seg_cap + 64u;
+    L.sq_cap[0] = 2u * L.seg_cap + 64u;
+  }
   L.chunk_cap = (uint32_t)(n / kRunChunk + L.run_cap + 2);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -150,6 +161,13 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = 0) {
   for (int c = 0; c < kSmallClasses; ++c) L.sq[c] = take((size_t)L.sq_cap[c] * sizeof(SmallSeg));
   L.runs = take((size_t)L.run_cap * sizeof(Run));
   L.chunkmap = take((size_t)L.chunk_cap * 4);
+  // a caller buffer that is element- but not 16-byte-aligned (a CUDA view
+  // with a storage offset, e.g. x[1:]) is sorted in an aligned copy: the
+  // partition pass writes whole runs with cp.async.bulk, which needs
+  // 16-byte-aligned global addresses
+  L.stage_keys = take(staged ? n * kb + 64 : 0);
+  L.stage_pay = take(staged && pay ? n * 4 + 64 : 0);
+  L.stage_out = take(export_records ? (size_t)L.seg_cap * sizeof(StageRecord) : 0);
   L.total = off;
   return L;
 }
@@ -158,10 +176,14 @@ struct GraphEntry {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraphNode_t init_node = nullptr;
-  cudaGraphConditionalHandle cond = 0;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaGraphConditionalHandle cond = 0, cond_outer = 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   cudaKernelNodeParams init_params;
 };
+
+static_assert(sizeof(StageRecord) == sizeof(tsq_stage_record), "stage record layout");
+static_assert(sizeof(tsq_params) == 64, "tsq_params layout (tests/test_api_cpu.py)");
+static_assert(sizeof(tsq_stats) == 168, "tsq_stats layout (tests/test_api_cpu.py)");
 
 }  // namespace
 
@@ -183,6 +205,7 @@ struct tsq_workspace {
   std::vector<float> level_ms, sched_ms;  // host_levels mode trace
   std::vector<uint64_t> level_bytes;
   std::vector<uint32_t> level_segs, level_tiles;
+  std::vector<tsq_stage_record> records;  // stage-export mode, one level
 };
 
 #define TSQ_CUDA(call)                                     \
@@ -196,6 +219,24 @@ struct tsq_workspace {
   } while (0)
 
 namespace {
+
+// Every entry point runs on the workspace's device and leaves the caller's
+// current device as it found it.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem, int block = kThreads) {
   int occ = 0;
@@ -240,6 +281,22 @@ cudaError_t launch_level(const KernelSet &ks, const LevelLaunch &L, Params **dst
   return cudaLaunchKernel(ks.sched, L.sched_grid, dim3(kThreads), args, ks.sched_smem, s);
 }
 
+// the on-chip sort classes, retirement and the queue reset (a drain round)
+cudaError_t launch_drain(tsq_workspace *ws, const KernelSet &ks, Params **dst, cudaStream_t s) {
+  void *args[1] = {dst};
+  for (int c = 0; c < kSmallClasses; ++c) {
+    cudaError_t e = cudaLaunchKernel(
+        ks.small[c], dim3(occupancy_grid(ws, ks.small[c], ks.small_smem[c], ks.small_threads[c])),
+        dim3(ks.small_threads[c]), args, ks.small_smem[c], s);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)),
+                                   dim3(kThreads), args, 0, s);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernel(reinterpret_cast<const void *>(&drain_kernel), dim3(1), dim3(32), args,
+                          0, s);
+}
+
 void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void *payload,
                  size_t n) {
   memset(p, 0, sizeof(*p));
@@ -281,15 +338,23 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
   p->reproducible = 0;
 }
 
+// The whole sort as one graph, no host round trip per level:
+//   init -> WHILE(outer) { WHILE(inner) { partition -> schedule }
+//                          -> small sorts || retire -> drain }
+// The last schedule CTA of a level keeps the inner loop going while
+// segments remain; when the on-chip or run queues could not take another
+// level it ends the inner loop early (a flush), the drain round empties
+// them and the outer loop re-enters the level loop.  Normally the outer
+// body runs once.
 tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   KernelSet ks;
   if (!get_set(kt, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
   tsq_status st = prepare_small_smem(ks);
   if (st != TSQ_OK) return st;
-  for (int i = 0; i < 4; ++i) TSQ_CUDA(cudaEventCreate(&ge->ev[i]));
+  for (int i = 0; i < 3; ++i) TSQ_CUDA(cudaEventCreate(&ge->ev[i]));
   TSQ_CUDA(cudaGraphCreate(&ge->graph, 0));
   cudaGraph_t g = ge->graph;
-  cudaGraphNode_t e0, e1, e2, e3, cnode, lnode, rnode;
+  cudaGraphNode_t e0, e1, e2, onode, inode, lnode, schednode;
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e0, g, nullptr, 0, ge->ev[0]));
 
   static Params dummy;  // replaced per call via cudaGraphExecKernelNodeSetParams
@@ -306,17 +371,30 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   TSQ_CUDA(cudaGraphAddKernelNode(&ge->init_node, g, &e0, 1, &ge->init_params));
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e1, g, &ge->init_node, 1, ge->ev[1]));
 
-  TSQ_CUDA(cudaGraphConditionalHandleCreate(&ge->cond, g, 0, cudaGraphCondAssignDefault));
+  // both handles live in the top-level graph: the outer one enters its body
+  // once per launch by default; the init kernel sets the inner one
+  TSQ_CUDA(cudaGraphConditionalHandleCreate(&ge->cond_outer, g, 1, cudaGraphCondAssignDefault));
+  TSQ_CUDA(cudaGraphConditionalHandleCreate(&ge->cond, g, 0, 0));
   // cudaGraphNodeParams has a deleted default constructor (union member)
-  alignas(cudaGraphNodeParams) unsigned char cp_raw[sizeof(cudaGraphNodeParams)];
-  memset(cp_raw, 0, sizeof(cp_raw));
-  cudaGraphNodeParams &cp = *reinterpret_cast<cudaGraphNodeParams *>(cp_raw);
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = ge->cond;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  TSQ_CUDA(cudaGraphAddNode(&cnode, g, &e1, 1, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  alignas(cudaGraphNodeParams) unsigned char op_raw[sizeof(cudaGraphNodeParams)];
+  memset(op_raw, 0, sizeof(op_raw));
+  cudaGraphNodeParams &op = *reinterpret_cast<cudaGraphNodeParams *>(op_raw);
+  op.type = cudaGraphNodeTypeConditional;
+  op.conditional.handle = ge->cond_outer;
+  op.conditional.type = cudaGraphCondTypeWhile;
+  op.conditional.size = 1;
+  TSQ_CUDA(cudaGraphAddNode(&onode, g, &e1, 1, &op));
+  cudaGraph_t obody = op.conditional.phGraph_out[0];
+
+  alignas(cudaGraphNodeParams) unsigned char ip_raw[sizeof(cudaGraphNodeParams)];
+  memset(ip_raw, 0, sizeof(ip_raw));
+  cudaGraphNodeParams &ip = *reinterpret_cast<cudaGraphNodeParams *>(ip_raw);
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = ge->cond;
+  ip.conditional.type = cudaGraphCondTypeWhile;
+  ip.conditional.size = 1;
+  TSQ_CUDA(cudaGraphAddNode(&inode, obody, nullptr, 0, &ip));
+  cudaGraph_t body = ip.conditional.phGraph_out[0];
 
   Params *dp = ws->d_params;
   void *dev_args[1] = {&dp};
@@ -334,9 +412,7 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   lk.blockDim = dim3(kThreads);
   lk.sharedMemBytes = (unsigned)ks.sched_smem;
   lk.kernelParams = dev_args;
-  cudaGraphNode_t schednode;
   TSQ_CUDA(cudaGraphAddKernelNode(&schednode, body, &lnode, 1, &lk));
-  TSQ_CUDA(cudaGraphAddEventRecordNode(&e2, g, &cnode, 1, ge->ev[2]));
 
   cudaGraphNode_t tail[kSmallClasses + 1];
   for (int c = 0; c < kSmallClasses; ++c) {
@@ -345,26 +421,34 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
     sk.gridDim = dim3(occupancy_grid(ws, ks.small[c], ks.small_smem[c], ks.small_threads[c]));
     sk.blockDim = dim3(ks.small_threads[c]);
     sk.sharedMemBytes = (unsigned)ks.small_smem[c];
-    TSQ_CUDA(cudaGraphAddKernelNode(&tail[c], g, &e2, 1, &sk));
+    TSQ_CUDA(cudaGraphAddKernelNode(&tail[c], obody, &inode, 1, &sk));
   }
   cudaKernelNodeParams rk = lk;
   rk.func = const_cast<void *>(ks.retire);
   rk.gridDim = dim3(occupancy_grid(ws, ks.retire, 0));
   rk.sharedMemBytes = 0;
-  TSQ_CUDA(cudaGraphAddKernelNode(&rnode, g, &e2, 1, &rk));
-  tail[kSmallClasses] = rnode;
-  TSQ_CUDA(cudaGraphAddEventRecordNode(&e3, g, tail, kSmallClasses + 1, ge->ev[3]));
+  TSQ_CUDA(cudaGraphAddKernelNode(&tail[kSmallClasses], obody, &inode, 1, &rk));
+  cudaKernelNodeParams dk = lk;
+  dk.func = reinterpret_cast<void *>(&drain_kernel);
+  dk.gridDim = dim3(1);
+  dk.blockDim = dim3(32);
+  dk.sharedMemBytes = 0;
+  cudaGraphNode_t dnode;
+  TSQ_CUDA(cudaGraphAddKernelNode(&dnode, obody, tail, kSmallClasses + 1, &dk));
+  TSQ_CUDA(cudaGraphAddEventRecordNode(&e2, g, &onode, 1, ge->ev[2]));
   TSQ_CUDA(cudaGraphInstantiate(&ge->exec, g, 0));
   return TSQ_OK;
 }
 
-tsq_status reserve_locked(tsq_workspace *ws, size_t n, int kt, int pt, int small_t = 0) {
-  const Layout L = make_layout(n, kt, pt, small_t);
+tsq_status reserve_locked(tsq_workspace *ws, size_t n, int kt, int pt, int small_t = 0,
+                          bool staged = false, bool export_records = false) {
+  const Layout L = make_layout(n, kt, pt, small_t, staged, export_records);
   if (L.total <= ws->block_bytes) {
     if (n > ws->cap_elems) ws->cap_elems = n;
     return TSQ_OK;
   }
   if (ws->block) {
+    cudaEventSynchronize(ws->done);
     cudaFree(ws->block);
     ws->block = nullptr;
     ws->block_bytes = 0;
@@ -390,6 +474,11 @@ tsq_status check_args(size_t n, int kt, int pt) {
   return TSQ_OK;
 }
 
+// element alignment of a caller buffer is required; 16-byte alignment is
+// not (a misaligned buffer is sorted through an aligned copy)
+bool element_aligned(const void *p, size_t bytes) { return p == nullptr || (uintptr_t)p % bytes == 0; }
+bool bulk_aligned(const void *p) { return p == nullptr || (uintptr_t)p % 16 == 0; }
+
 // The control block comes back through mapped host memory written by a tiny
 // kernel, not a memcpy: a copy would queue on the copy engine behind any
 // large device->host transfer in flight on other streams (sort_many's
@@ -402,6 +491,12 @@ tsq_status read_ctl(tsq_workspace *ws, cudaStream_t s) {
   return TSQ_OK;
 }
 
+tsq_status status_of(uint32_t error) {
+  if (error & (ERR_DEPTH | ERR_LEVELS)) return TSQ_ERR_DEPTH_EXCEEDED;
+  if (error) return TSQ_ERR_CAPACITY;
+  return TSQ_OK;
+}
+
 tsq_status fill_stats(tsq_workspace *ws, size_t n, tsq_stats *st) {
   const Ctl &c = *ws->h_ctl;
   memset(st, 0, sizeof(*st));
@@ -409,7 +504,7 @@ tsq_status fill_stats(tsq_workspace *ws, size_t n, tsq_stats *st) {
   st->stages = c.stages;
   st->levels = c.levels;
   st->max_depth = c.max_depth;
-  st->small_segments = 0;
+  st->small_segments = c.small_segs_done;
   for (int q = 0; q < kSmallClasses; ++q) st->small_segments += c.sq_count[q];
   st->eq_runs = c.eq_runs;
   st->eq_elements = c.eq_elements;
@@ -424,9 +519,9 @@ tsq_status fill_stats(tsq_workspace *ws, size_t n, tsq_stats *st) {
   st->error_flags = c.error;
   st->writes_caller = c.writes0;
   st->writes_workspace = c.writes1;
-  if (c.error & ERR_DEPTH) return TSQ_ERR_DEPTH_EXCEEDED;
-  if (c.error) return TSQ_ERR_CAPACITY;
-  return TSQ_OK;
+  st->bisected = c.bisected;
+  st->flushes = c.flushes;
+  return status_of(c.error);
 }
 
 struct ActiveGuard {
@@ -445,6 +540,18 @@ tsq_status acquire(tsq_workspace *ws) {
   return TSQ_OK;
 }
 
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// default depth guard: max(24, 2 * ceil(log2 n)) levels of sampled pivots
+int default_max_depth(size_t n) {
+  int lg = 0;
+  while (lg < 63 && (1ull << lg) < n) ++lg;
+  return 2 * lg > 24 ? 2 * lg : 24;
+}
+
 }  // namespace
 
 extern "C" {
@@ -455,7 +562,7 @@ const char *tsq_status_str(tsq_status s) {
     case TSQ_ERR_ALLOC: return "device workspace allocation failed";
     case TSQ_ERR_UNSUPPORTED_DTYPE: return "unsupported dtype";
     case TSQ_ERR_CUDA: return "CUDA error";
-    case TSQ_ERR_DEPTH_EXCEEDED: return "recursion depth guard exceeded";
+    case TSQ_ERR_DEPTH_EXCEEDED: return "recursion level limit reached";
     case TSQ_ERR_INVALID: return "invalid argument";
     case TSQ_ERR_BUSY: return "sorter instance is not reentrant";
     case TSQ_ERR_CAPACITY: return "device queue capacity exceeded";
@@ -468,7 +575,8 @@ int tsq_abi_version(void) { return TSQ_ABI_VERSION; }
 tsq_status tsq_workspace_create(tsq_workspace **out, int device) {
   if (!out) return TSQ_ERR_INVALID;
   *out = nullptr;
-  TSQ_CUDA(cudaSetDevice(device));
+  DeviceGuard dg(device);
+  if (!dg.ok) return TSQ_ERR_CUDA;
   tsq_workspace *ws = new tsq_workspace();
   ws->device = device;
   cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -489,8 +597,8 @@ tsq_status tsq_workspace_create(tsq_workspace **out, int device) {
 
 void tsq_workspace_destroy(tsq_workspace *ws) {
   if (!ws) return;
-  cudaSetDevice(ws->device);
-  cudaDeviceSynchronize();
+  DeviceGuard dg(ws->device);
+  if (ws->done) cudaEventSynchronize(ws->done);
   for (auto &kv : ws->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
@@ -518,7 +626,7 @@ tsq_status tsq_workspace_reserve(tsq_workspace *ws, size_t n, tsq_dtype key_t,
   st = acquire(ws);
   if (st != TSQ_OK) return st;
   ActiveGuard g(ws);
-  cudaSetDevice(ws->device);
+  DeviceGuard dg(ws->device);
   return reserve_locked(ws, n, key_t, payload_t);
 }
 
@@ -527,7 +635,7 @@ tsq_status tsq_workspace_free(tsq_workspace *ws) {
   tsq_status st = acquire(ws);
   if (st != TSQ_OK) return st;
   ActiveGuard g(ws);
-  cudaSetDevice(ws->device);
+  DeviceGuard dg(ws->device);
   if (ws->block) {
     cudaEventSynchronize(ws->done);
     cudaFree(ws->block);
@@ -541,6 +649,19 @@ tsq_status tsq_workspace_free(tsq_workspace *ws) {
 size_t tsq_workspace_capacity(const tsq_workspace *ws) { return ws ? ws->cap_elems : 0; }
 uint64_t tsq_workspace_alloc_count(const tsq_workspace *ws) { return ws ? ws->alloc_count : 0; }
 
+tsq_status tsq_workspace_last_status(tsq_workspace *ws, void *stream) {
+  if (!ws) return TSQ_ERR_INVALID;
+  tsq_status st = acquire(ws);
+  if (st != TSQ_OK) return st;
+  ActiveGuard g(ws);
+  DeviceGuard dg(ws->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  TSQ_CUDA(cudaStreamWaitEvent(s, ws->done, 0));
+  st = read_ctl(ws, s);
+  if (st != TSQ_OK) return st;
+  return status_of(ws->h_ctl->error);
+}
+
 tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dtype payload_t,
                     const tsq_params *params, tsq_workspace *ws, void *stream,
                     tsq_stats *stats) {
@@ -549,10 +670,14 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   if (st != TSQ_OK) return st;
   if ((payload_t == TSQ_U32) != (payload != nullptr)) return TSQ_ERR_INVALID;
   if (n > 0 && !keys) return TSQ_ERR_INVALID;
+  const int kb = key_bytes_of(key_t);
+  if (!element_aligned(keys, kb) || !element_aligned(payload, 4)) return TSQ_ERR_INVALID;
   st = acquire(ws);
   if (st != TSQ_OK) return st;
   ActiveGuard guard(ws);
-  TSQ_CUDA(cudaSetDevice(ws->device));
+  DeviceGuard dg(ws->device);
+  if (!dg.ok) return TSQ_ERR_CUDA;
+  NvtxRange nvtx("tsq_sort");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n <= 1) {
@@ -562,35 +687,59 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   const bool pay = payload_t == TSQ_U32;
   KernelSet ks;
   if (!get_set(key_t, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
-  int small_t = default_small_t(key_t, payload_t, n);
-#ifdef TSQ_SMALL_T
-  small_t = TSQ_SMALL_T;
-#endif
-  if (params && params->small_threshold > 0)
-    small_t = params->small_threshold < ks.small_cap[1] ? params->small_threshold : ks.small_cap[1];
-  // allocation precedes any mutation (core.py:1599, TempAllocationError)
-  st = reserve_locked(ws, n, key_t, payload_t, small_t);
-  if (st != TSQ_OK) return st;
-  const Layout L = make_layout(n, key_t, payload_t, small_t);
-  Params pv;
-  fill_params(ws, L, &pv, keys, payload, n);
-  pv.small_t = small_t;
-  pv.raw[1] = ks.raw_order ? 1 : 0;
-  for (int c = 0; c < kSmallClasses; ++c) pv.sq_lim[c] = ks.small_cap[c];
   tsq_params defaults;
   memset(&defaults, 0, sizeof(defaults));
   defaults.mitigation = 1;
   defaults.fast_paths = 1;
   const tsq_params &pp = params ? *params : defaults;
+  int small_t = default_small_t(key_t, payload_t, n);
+#ifdef TSQ_SMALL_T
+  small_t = TSQ_SMALL_T;
+#endif
+  if (pp.small_threshold > 0)
+    small_t = pp.small_threshold < ks.small_cap[1] ? pp.small_threshold : ks.small_cap[1];
+  // stage export: host-driven levels, the sort in an internal copy, the
+  // caller's buffers a view of each level's post-stage state
+  const bool exporting = pp.stage_export != 0;
+  const bool staged = exporting || !bulk_aligned(keys) || !bulk_aligned(payload);
+  const bool host_levels = pp.host_levels || exporting;
+  // allocation precedes any mutation (core.py:1599, TempAllocationError)
+  st = reserve_locked(ws, n, key_t, payload_t, small_t, staged, exporting);
+  if (st != TSQ_OK) return st;
+  const Layout L = make_layout(n, key_t, payload_t, small_t, staged, exporting);
+  char *base = reinterpret_cast<char *>(ws->block);
+  void *skeys = staged ? base + L.stage_keys : keys;
+  void *spay = staged && pay ? base + L.stage_pay : payload;
+  Params pv;
+  fill_params(ws, L, &pv, skeys, spay, n);
+  pv.small_t = small_t;
+  pv.raw[1] = ks.raw_order ? 1 : 0;
+  for (int c = 0; c < kSmallClasses; ++c) pv.sq_lim[c] = ks.small_cap[c];
   pv.dran = pp.dran > 0.0 ? pp.dran : 1.0;
   pv.mitigation = pp.mitigation;
   pv.fast_paths = pp.fast_paths;
   pv.reproducible = pp.reproducible != 0;
-  pv.max_depth = pp.max_depth > 0 ? pp.max_depth : 96;
+  pv.max_depth = pp.max_depth > 0 ? pp.max_depth : default_max_depth(n);
+  if (exporting) {
+    pv.view_keys = keys;
+    pv.view_pay = reinterpret_cast<uint32_t *>(payload);
+    pv.stage_out = reinterpret_cast<StageRecord *>(base + L.stage_out);
+  }
   TSQ_CUDA(cudaStreamWaitEvent(s, ws->done, 0));
+  if (staged) {
+    TSQ_CUDA(cudaMemcpyAsync(skeys, keys, n * kb, cudaMemcpyDeviceToDevice, s));
+    if (pay) TSQ_CUDA(cudaMemcpyAsync(spay, payload, n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  auto stage_back = [&]() -> tsq_status {
+    if (staged) {
+      TSQ_CUDA(cudaMemcpyAsync(keys, skeys, n * kb, cudaMemcpyDeviceToDevice, s));
+      if (pay) TSQ_CUDA(cudaMemcpyAsync(payload, spay, n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    return TSQ_OK;
+  };
 
   const int gkey = key_t * 2 + (pay ? 1 : 0);
-  if (!pp.host_levels) {
+  if (!host_levels) {
     GraphEntry &ge = ws->graphs[gkey];
     if (!ge.exec) {
       st = build_graph(ws, key_t, pay, &ge);
@@ -601,35 +750,42 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     }
     pv.use_cond = 1;
     pv.cond = ge.cond;
+    pv.cond_outer = ge.cond_outer;
     Params *dst = ws->d_params;
     void *args[2] = {&pv, &dst};
     cudaKernelNodeParams kp = ge.init_params;
     kp.kernelParams = args;
     TSQ_CUDA(cudaGraphExecKernelNodeSetParams(ge.exec, ge.init_node, &kp));
     TSQ_CUDA(cudaGraphLaunch(ge.exec, s));
+    st = stage_back();
+    if (st != TSQ_OK) return st;
     TSQ_CUDA(cudaEventRecord(ws->done, s));
     if (stats) {
       st = read_ctl(ws, s);
       if (st != TSQ_OK) return st;
       st = fill_stats(ws, n, stats);
       cudaEventElapsedTime(&stats->ms_levels, ge.ev[1], ge.ev[2]);
-      cudaEventElapsedTime(&stats->ms_total, ge.ev[0], ge.ev[3]);
+      cudaEventElapsedTime(&stats->ms_total, ge.ev[0], ge.ev[2]);
       return st;
     }
     return TSQ_OK;
   }
 
   // host-driven levels: same kernels, one launch per level with a read-back
-  // of the queue size in between (per-level timing / trace)
+  // of the queue size in between (per-level timing / trace / stage export)
   st = prepare_small_smem(ks);
   if (st != TSQ_OK) return st;
+  TSQ_CUDA(cudaFuncSetAttribute(ks.exportk, cudaFuncAttributeMaxDynamicSharedMemorySize, 0));
   pv.use_cond = 0;
-  cudaEvent_t e0, em, e1, t0, t1;
-  TSQ_CUDA(cudaEventCreate(&e0));
-  TSQ_CUDA(cudaEventCreate(&em));
-  TSQ_CUDA(cudaEventCreate(&e1));
-  TSQ_CUDA(cudaEventCreate(&t0));
-  TSQ_CUDA(cudaEventCreate(&t1));
+  struct Events {
+    cudaEvent_t e[5] = {};
+    ~Events() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } ev;
+  for (auto &x : ev.e) TSQ_CUDA(cudaEventCreate(&x));
+  cudaEvent_t &e0 = ev.e[0], &em = ev.e[1], &e1 = ev.e[2], &t0 = ev.e[3], &t1 = ev.e[4];
   ws->level_ms.clear();
   ws->sched_ms.clear();
   ws->level_segs.clear();
@@ -650,16 +806,29 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
       ws->level_bytes.push_back(ws->h_ctl->bytes_partition - bytes_before);
       bytes_before = ws->h_ctl->bytes_partition;
     }
+    if (ws->h_ctl->flush) {  // the queues are near full: drain them, then go on
+      TSQ_CUDA(launch_drain(ws, ks, &dst, s));
+      st = read_ctl(ws, s);
+      if (st != TSQ_OK) return st;
+    }
     if (getenv("TSQ_DEBUG_LEVELS"))
       fprintf(stderr, "tsq level %d: segments %u tiles %u small %u/%u runs %u error %u\n", lv,
               ws->h_ctl->cur_nseg, ws->h_ctl->cur_ntiles, ws->h_ctl->sq_count[0],
               ws->h_ctl->sq_count[1], (uint32_t)(ws->h_ctl->run_packed >> 32), ws->h_ctl->error);
     if (ws->h_ctl->cur_nseg == 0 || ws->h_ctl->error) break;
-    ws->level_segs.push_back(ws->h_ctl->cur_nseg);
+    const uint32_t nseg = ws->h_ctl->cur_nseg;
+    ws->level_segs.push_back(nseg);
     ws->level_tiles.push_back(ws->h_ctl->cur_ntiles);
+    char name[32];
+    snprintf(name, sizeof(name), "tsq level %d", lv);
+    NvtxRange lvl(name);
     TSQ_CUDA(cudaEventRecord(e0, s));
     TSQ_CUDA(cudaLaunchKernel(ks.part, LL.part_grid, dim3(kPartThreads), largs, ks.part_smem, s));
     TSQ_CUDA(cudaEventRecord(em, s));
+    if (exporting) {
+      const unsigned g = nseg < 4u * (unsigned)ws->num_sms ? nseg : 4u * (unsigned)ws->num_sms;
+      TSQ_CUDA(cudaLaunchKernel(ks.exportk, dim3(g), dim3(kThreads), largs, 0, s));
+    }
     TSQ_CUDA(cudaLaunchKernel(ks.sched, LL.sched_grid, dim3(kThreads), largs, ks.sched_smem, s));
     TSQ_CUDA(cudaEventRecord(e1, s));
     TSQ_CUDA(cudaEventSynchronize(e1));
@@ -669,13 +838,17 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     ws->level_ms.push_back(ms);
     ws->sched_ms.push_back(ms2);
     total_levels += ms + ms2;
+    if (exporting) {
+      ws->records.resize(nseg);
+      TSQ_CUDA(cudaMemcpyAsync(ws->records.data(), pv.stage_out, nseg * sizeof(StageRecord),
+                               cudaMemcpyDeviceToHost, s));
+      TSQ_CUDA(cudaStreamSynchronize(s));
+      if (pp.on_level) pp.on_level(pp.on_level_user, lv, ws->records.data(), nseg);
+    }
   }
-  for (int c = 0; c < kSmallClasses; ++c)
-    TSQ_CUDA(cudaLaunchKernel(
-        ks.small[c], dim3(occupancy_grid(ws, ks.small[c], ks.small_smem[c], ks.small_threads[c])),
-        dim3(ks.small_threads[c]), largs, ks.small_smem[c], s));
-  TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
-                            largs, 0, s));
+  TSQ_CUDA(launch_drain(ws, ks, &dst, s));
+  st = stage_back();
+  if (st != TSQ_OK) return st;
   TSQ_CUDA(cudaEventRecord(t1, s));
   TSQ_CUDA(cudaEventRecord(ws->done, s));
   st = read_ctl(ws, s);
@@ -683,14 +856,9 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     st = fill_stats(ws, n, stats);
     stats->ms_levels = total_levels;
     cudaEventElapsedTime(&stats->ms_total, t0, t1);
-  } else if (st == TSQ_OK && ws->h_ctl->error) {
-    st = (ws->h_ctl->error & ERR_DEPTH) ? TSQ_ERR_DEPTH_EXCEEDED : TSQ_ERR_CAPACITY;
+  } else if (st == TSQ_OK) {
+    st = status_of(ws->h_ctl->error);
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(em);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
   return st;
 }
 
@@ -717,6 +885,10 @@ tsq_status tsq_partition_segment(const void *keys, const void *payload, void *ou
   if (st != TSQ_OK) return st;
   const bool pay = payload_t == TSQ_U32;
   if (pay != (payload != nullptr) || pay != (out_payload != nullptr)) return TSQ_ERR_INVALID;
+  const int kb = key_bytes_of(key_t);
+  if (!element_aligned(keys, kb) || !element_aligned(out_keys, kb) ||
+      !element_aligned(payload, 4) || !element_aligned(out_payload, 4))
+    return TSQ_ERR_INVALID;
   if (n == 0) {
     *new_l = -1;
     *new_r = 0;
@@ -725,19 +897,25 @@ tsq_status tsq_partition_segment(const void *keys, const void *payload, void *ou
   st = acquire(ws);
   if (st != TSQ_OK) return st;
   ActiveGuard guard(ws);
-  TSQ_CUDA(cudaSetDevice(ws->device));
+  DeviceGuard dg(ws->device);
+  if (!dg.ok) return TSQ_ERR_CUDA;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  st = reserve_locked(ws, n, key_t, payload_t);
+  // a misaligned output is written through an aligned copy (bulk stores)
+  const bool staged = !bulk_aligned(out_keys) || !bulk_aligned(out_payload);
+  st = reserve_locked(ws, n, key_t, payload_t, 0, staged);
   if (st != TSQ_OK) return st;
   KernelSet ks;
   if (!get_set(key_t, pay, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;
-  const Layout L = make_layout(n, key_t, payload_t);
+  const Layout L = make_layout(n, key_t, payload_t, 0, staged);
+  char *base = reinterpret_cast<char *>(ws->block);
+  void *ok = staged ? base + L.stage_keys : out_keys;
+  void *op = staged && pay ? base + L.stage_pay : out_payload;
   Params pv;
-  fill_params(ws, L, &pv, out_keys, out_payload, n);
+  fill_params(ws, L, &pv, ok, op, n);
   pv.keys[1] = const_cast<void *>(keys);
   pv.pay[1] = reinterpret_cast<uint32_t *>(const_cast<void *>(payload));
   pv.raw[1] = 1;
-  pv.aligned[1] = ((uintptr_t)keys % 16 == 0) && ((uintptr_t)payload % 16 == 0);
+  pv.aligned[1] = bulk_aligned(keys) && bulk_aligned(payload);
   pv.single_stage = 1;
   pv.given_pivot = host_enc(key_t, pivot);
   pv.use_cond = 0;
@@ -751,6 +929,10 @@ tsq_status tsq_partition_segment(const void *keys, const void *payload, void *ou
   TSQ_CUDA(launch_level(ks, level_launch(ws, ks), &dst, s));
   TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
                             largs, 0, s));
+  if (staged) {
+    TSQ_CUDA(cudaMemcpyAsync(out_keys, ok, n * kb, cudaMemcpyDeviceToDevice, s));
+    if (pay) TSQ_CUDA(cudaMemcpyAsync(out_payload, op, n * 4, cudaMemcpyDeviceToDevice, s));
+  }
   TSQ_CUDA(cudaEventRecord(ws->done, s));
   st = read_ctl(ws, s);
   if (st != TSQ_OK) return st;
@@ -767,10 +949,12 @@ tsq_status tsq_select_pivot(const void *keys, size_t n, tsq_dtype key_t, double 
   tsq_status st = check_args(n, key_t, TSQ_NONE);
   if (st != TSQ_OK) return st;
   if (n < 2) return TSQ_ERR_INVALID;
+  if (!element_aligned(keys, key_bytes_of(key_t))) return TSQ_ERR_INVALID;
   st = acquire(ws);
   if (st != TSQ_OK) return st;
   ActiveGuard guard(ws);
-  TSQ_CUDA(cudaSetDevice(ws->device));
+  DeviceGuard dg(ws->device);
+  if (!dg.ok) return TSQ_ERR_CUDA;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   KernelSet ks;
   if (!get_set(key_t, false, &ks)) return TSQ_ERR_UNSUPPORTED_DTYPE;

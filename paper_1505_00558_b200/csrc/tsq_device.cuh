@@ -26,7 +26,8 @@ constexpr int kSmallHuge = 16384;    // on-chip sort, 512-thread class, 4-byte k
 constexpr int kSmallClasses = 2;
 constexpr int kMaxSample = 1023;     // pivot sample size cap (2^10 - 1)
 constexpr int kRunChunk = 8192;      // elements per retire work item
-constexpr int kMaxLevels = 200;      // hard stop for the level loop
+constexpr int kMaxLevels = 512;      // hard stop for the level loop (never reached: the
+                                     // depth guard bisects key bounds, see Seg::klo)
 
 constexpr u64 kFlagAgg = 1ull << 62;  // look-back: tile aggregate published
 constexpr u64 kFlagInc = 2ull << 62;  // look-back: inclusive prefix published
@@ -43,10 +44,16 @@ enum ErrFlag : uint32_t { ERR_DEPTH = 1u, ERR_CAPACITY = 2u, ERR_LEVELS = 4u };
 
 // A live segment of one level: [begin, end) of buffer `buf` (0 = the
 // caller's keys, 1 = the workspace partner), partitioned around `pivot`
-// (an encoded key) or verified sorted / reversed.
+// (an encoded key) or verified sorted / reversed.  [klo, khi] bounds its
+// encoded keys: the root's is the whole key space, a < child's is
+// [klo, pivot - 1] and a > child's [pivot + 1, khi].  Beyond the depth
+// guard a segment is split at the bound's midpoint instead of a sampled
+// pivot, which halves the bound every level -- the recursion always ends
+// (the reference's _range always finishes, core.py:1643-1728).
 struct Seg {
   long long begin, end;
   u64 pivot;
+  u64 klo, khi;
   uint32_t tile_base, ntiles;
   uint32_t buf, kind, depth, noverify;
   uint32_t eq_fill;  // records, atomic placement: == payload slots reserved so far
@@ -87,6 +94,12 @@ struct Ctl {
   u64 bytes_partition, bytes_small, bytes_retire;
   u64 stage_lt, stage_gt;   // single-stage / select-pivot results
   u64 writes0, writes1;     // element writes into buffer 0 / workspace
+  // queue flushes: when the small-sort or run queues could not take one more
+  // level's appends, the level loop pauses, the on-chip sort and retire
+  // kernels drain them, and the loop resumes (so they never overflow)
+  uint32_t flush, flushes;
+  u64 small_segs_done;      // on-chip segments of earlier flush rounds
+  u64 bisected;             // segments split at their key-bound midpoint
 };
 
 // Everything a kernel needs; lives in device memory, written by the init
@@ -114,7 +127,24 @@ struct Params {
   uint32_t sq_cap[kSmallClasses];
   uint32_t seg_cap, tile_cap, run_cap, chunk_cap;
   Ctl *ctl;
-  cudaGraphConditionalHandle cond;
+  cudaGraphConditionalHandle cond;        // inner loop: one recursion level per pass
+  cudaGraphConditionalHandle cond_outer;  // outer loop: levels, then a queue drain
+  // stage export (stage_hook / trace mode, host-driven levels only): after
+  // each level, every segment's post-stage contents are written into the
+  // caller's buffers (view_*) -- the sort itself runs in an aligned copy --
+  // and a per-segment record into `stage_out`
+  void *view_keys;
+  uint32_t *view_pay;
+  struct StageRecord *stage_out;
+};
+
+// One stage of a host-driven level, as reported to stage_hook / trace
+// (tsq_stage_record in include/tsq.h; core.py:1705-1710).
+struct StageRecord {
+  long long a, b, new_l, new_r;
+  u64 pivot;          // caller's encoding (raw bits)
+  int32_t kind;       // TSQ_STAGE_* (include/tsq.h)
+  int32_t depth;
 };
 
 // ---- optional per-tile timeline (profiling builds only: -DTSQ_TRACE) -------

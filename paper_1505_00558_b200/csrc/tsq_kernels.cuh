@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
     if (threadIdx.x == 0) {
       Seg s;
       s.begin = 0; s.end = n; s.pivot = piv;
+      s.klo = 0; s.khi = (u64)KeyMax<U>::v;  // the whole (encoded) key space
       s.tile_base = 0; s.ntiles = ntiles;
       s.buf = buf; s.kind = kind; s.depth = 1; s.noverify = 0; s.eq_fill = 0; s.fail = 0;
       pv.segs[0][0] = s;
@@ -163,6 +164,101 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
     }
   }
   if (threadIdx.x == 0 && pv.use_cond) cudaGraphSetConditional(pv.cond, more ? 1u : 0u);
+}
+
+// End of a drain round (after the on-chip sort and retire kernels have
+// consumed the queues): reset the queues, and resume the level loop if
+// segments remain (a flush paused it) or end the sort.
+__global__ void drain_kernel(const Params *__restrict__ P) {
+  Ctl *ctl = P->ctl;
+  if (threadIdx.x != 0) return;
+  ctl->small_segs_done += (u64)ctl->sq_count[0] + (u64)ctl->sq_count[1];
+  for (int c = 0; c < kSmallClasses; ++c) {
+    ctl->sq_count[c] = 0;
+    ctl->sq_ticket[c] = 0;
+  }
+  ctl->run_packed = 0;
+  ctl->run_ticket = 0;
+  const bool more = ctl->cur_nseg > 0 && ctl->error == 0;
+  if (more) ctl->flushes += 1;
+  ctl->flush = 0;
+  __threadfence();
+  if (P->use_cond) {
+    cudaGraphSetConditional(P->cond, more ? 1u : 0u);
+    cudaGraphSetConditional(P->cond_outer, more ? 1u : 0u);
+  }
+}
+
+// Stage export (stage_hook / trace mode, host-driven levels): between a
+// level's partition pass and its scheduling, write every segment's
+// post-stage contents into the caller's buffers (the view) and its record --
+// the state the reference's hook sees after each stage (core.py:1705-1710).
+// One CTA per segment; debug path, plain loads and stores.
+template <class C, bool PAY>
+__global__ void __launch_bounds__(kThreads) export_level_kernel(const Params *__restrict__ P) {
+  typedef typename C::U U;
+  __shared__ u64 s_cnt[2];
+  const Ctl *ctl = P->ctl;
+  const int cur = (int)(ctl->level & 1u);
+  const uint32_t nseg = ctl->cur_nseg;
+  U *vk = reinterpret_cast<U *>(P->view_keys);
+  uint32_t *vp = P->view_pay;
+  for (uint32_t sid = blockIdx.x; sid < nseg; sid += gridDim.x) {
+    const Seg sg = P->segs[cur][sid];
+    const long long b = sg.begin, e = sg.end, len = e - b;
+    const U praw = C::dec((U)sg.pivot);
+    StageRecord rec;
+    rec.a = b;
+    rec.b = e - 1;
+    rec.pivot = (u64)praw;
+    rec.depth = (int32_t)sg.depth;
+    rec.new_l = -1;
+    rec.new_r = -1;
+    if (sg.kind == KIND_PARTITION) {
+      const u64 inc = P->lookback[cur][sg.tile_base + (P->reproducible ? sg.ntiles - 1 : 0)];
+      const long long lt = (long long)((inc >> 31) & 0x7fffffffull);
+      const long long gt = (long long)(inc & 0x7fffffffull);
+      const int db = (int)sg.buf ^ 1;
+      const U *src = reinterpret_cast<const U *>(P->keys[db]);
+      const bool raw = P->raw[db] != 0;
+      for (long long i = threadIdx.x; i < len; i += kThreads) {
+        const bool mid = i >= lt && i < len - gt;
+        vk[b + i] = mid ? praw : (raw ? src[b + i] : C::dec(src[b + i]));
+        if (PAY) vp[b + i] = mid ? P->side_pay[b + (i - lt)] : P->pay[db][b + i];
+      }
+      rec.kind = TSQ_STAGE_PARTITION;
+      rec.new_l = b + lt - 1;
+      rec.new_r = e - gt;
+    } else if (sg.fail) {
+      rec.kind = TSQ_STAGE_HANDLER_FALLBACK;
+      rec.new_l = sg.kind == KIND_VERIFY_ASC ? TSQ_STAGE_SORTED : TSQ_STAGE_REVERSED;
+    } else {
+      // verified: the segment is sorted (or reversed) where it lies
+      const bool desc = sg.kind == KIND_VERIFY_DESC;
+      const U *src = reinterpret_cast<const U *>(P->keys[sg.buf]);
+      const bool raw = P->raw[sg.buf] != 0;
+      if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+      __syncthreads();
+      u64 lt = 0, gt = 0;
+      for (long long i = threadIdx.x; i < len; i += kThreads) {
+        const long long s = desc ? e - 1 - i : b + i;
+        const U x = src[s];
+        const U ex = raw ? C::enc(x) : x;
+        lt += ex < (U)sg.pivot ? 1 : 0;
+        gt += ex > (U)sg.pivot ? 1 : 0;
+        vk[b + i] = raw ? x : C::dec(x);
+        if (PAY) vp[b + i] = P->pay[sg.buf][s];
+      }
+      atomicAdd(&s_cnt[0], lt);
+      atomicAdd(&s_cnt[1], gt);
+      __syncthreads();
+      rec.kind = desc ? TSQ_STAGE_REVERSED : TSQ_STAGE_SORTED;
+      rec.new_l = b + (long long)s_cnt[0] - 1;
+      rec.new_r = e - (long long)s_cnt[1];
+    }
+    if (threadIdx.x == 0) P->stage_out[sid] = rec;
+    __syncthreads();
+  }
 }
 
 // Retire finished runs into buffer 0, chunk by chunk.

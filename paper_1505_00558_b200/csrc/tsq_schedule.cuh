@@ -20,8 +20,26 @@ namespace tsq {
 // per-CTA statistics (shared-memory atomics, one global flush per CTA)
 enum SchedStat {
   ST_STAGES, ST_SORTED, ST_REVERSED, ST_DEPTH, ST_BYTES_PART, ST_BYTES_RETIRE, ST_W0, ST_W1,
-  ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_COUNT
+  ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_BISECTED, ST_COUNT
 };
+
+// Key bounds of a segment's children (encoded keys): < child [klo, p - 1],
+// > child [p + 1, khi].  An empty side never gets scheduled, so the clamps
+// only keep the arithmetic in range.
+__device__ __forceinline__ void child_bounds(const Seg &sg, int c, u64 *lo, u64 *hi) {
+  if (c == 0) {
+    *lo = sg.klo;
+    *hi = sg.pivot > sg.klo ? sg.pivot - 1 : sg.klo;
+  } else {
+    *lo = sg.pivot < sg.khi ? sg.pivot + 1 : sg.khi;
+    *hi = sg.khi;
+  }
+}
+
+// Beyond the depth guard: split at the midpoint of the key bound.  Every
+// such level halves the bound, so a segment ends within key-bits levels
+// (all keys equal once klo == khi: one == p run).
+__device__ __forceinline__ u64 bisect_pivot(u64 lo, u64 hi) { return lo + ((hi - lo) >> 1); }
 
 #ifndef TSQ_WARP_SAMPLES
 #define TSQ_WARP_SAMPLES 127
@@ -339,7 +357,7 @@ __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u
 
 struct ReqLevel {  // a child queued for the next level
   long long begin, end;
-  u64 pivot;
+  u64 pivot, klo, khi;
   uint32_t buf, kind, depth, noverify, ntiles, valid;
 };
 struct ReqRun {
@@ -388,6 +406,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         if (requeue) {
           ReqLevel &q = rs.lv[warp][0];
           q.begin = sg.begin; q.end = sg.end; q.pivot = sg.pivot; q.buf = sg.buf;
+          q.klo = sg.klo; q.khi = sg.khi;
           q.kind = KIND_PARTITION; q.depth = sg.depth; q.noverify = 1;
           q.ntiles = tiles_of<C, PAY>(sg.begin, sg.end); q.valid = 1;
         } else if (sg.fail == 0) {
@@ -418,18 +437,25 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
           q.begin = cb; q.len = cl; q.buf = db; q.valid = 1;
           atomicMax(&st[ST_DEPTH], (u64)depth);
         }
-      } else if ((int)depth > P->max_depth) {
-        if (lane == 0) atomicOr(&P->ctl->error, (uint32_t)ERR_DEPTH);
       } else {
+        u64 klo, khi;
+        child_bounds(sg, c, &klo, &khi);
         int flag = 0;
-        const U piv = warp_select_pivot<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
-                                           cb, cl, P->dran, P->mitigation, &flag);
+        u64 piv;
+        if ((int)depth > P->max_depth) {  // depth guard: bisect the key bound
+          piv = bisect_pivot(klo, khi);
+          if (lane == 0) atomicAdd(&st[ST_BISECTED], 1ull);
+        } else {
+          piv = (u64)warp_select_pivot<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
+                                          cb, cl, P->dran, P->mitigation, &flag);
+        }
         if (lane == 0) {
           uint32_t kind = KIND_PARTITION;
           if (P->fast_paths)
             kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
           ReqLevel &q = rs.lv[warp][0];
-          q.begin = cb; q.end = cb + cl; q.pivot = (u64)piv; q.buf = db; q.kind = kind;
+          q.klo = klo; q.khi = khi;
+          q.begin = cb; q.end = cb + cl; q.pivot = piv; q.buf = db; q.kind = kind;
           q.depth = depth; q.noverify = 0; q.ntiles = tiles_of<C, PAY>(cb, cb + cl); q.valid = 1;
         }
       }
@@ -496,6 +522,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         if (lane == 0) {
           Seg s;
           s.begin = q.begin; s.end = q.end; s.pivot = q.pivot;
+          s.klo = q.klo; s.khi = q.khi;
           s.tile_base = ltile; s.ntiles = q.ntiles;
           s.buf = q.buf; s.kind = q.kind; s.depth = q.depth; s.noverify = q.noverify;
           s.eq_fill = 0; s.fail = 0;
@@ -535,8 +562,8 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
 // CTA-wide appends (CTA mode: few segments, no contention to aggregate)
 template <class C, bool PAY>
 __device__ void cta_append_level(const Params *P, int nxt, long long begin, long long end,
-                                 uint32_t buf, u64 pivot, uint32_t kind, uint32_t depth,
-                                 uint32_t noverify, volatile uint32_t *bc) {
+                                 uint32_t buf, u64 pivot, u64 klo, u64 khi, uint32_t kind,
+                                 uint32_t depth, uint32_t noverify, volatile uint32_t *bc) {
   const uint32_t ntiles = tiles_of<C, PAY>(begin, end);
   if (threadIdx.x == 0) {
     Ctl *ctl = P->ctl;
@@ -546,6 +573,7 @@ __device__ void cta_append_level(const Params *P, int nxt, long long begin, long
     if (slot < P->seg_cap && (u64)tbase + ntiles <= P->tile_cap) {
       Seg s;
       s.begin = begin; s.end = end; s.pivot = pivot;
+      s.klo = klo; s.khi = khi;
       s.tile_base = tbase; s.ntiles = ntiles;
       s.buf = buf; s.kind = kind; s.depth = depth; s.noverify = noverify;
       s.eq_fill = 0; s.fail = 0;
@@ -615,8 +643,8 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
     if (!kids) return;
   } else if (sg.kind != KIND_PARTITION) {
     if (requeue) {
-      cta_append_level<C, PAY>(P, nxt, sg.begin, sg.end, sg.buf, sg.pivot, KIND_PARTITION,
-                               sg.depth, 1, bc);
+      cta_append_level<C, PAY>(P, nxt, sg.begin, sg.end, sg.buf, sg.pivot, sg.klo, sg.khi,
+                               KIND_PARTITION, sg.depth, 1, bc);
     } else {
       const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
       if (!(rk == RUN_SORTED && sg.buf == 0))
@@ -642,18 +670,21 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
       }
       return;
     }
-    if ((int)depth > P->max_depth) {
-      if (threadIdx.x == 0) atomicOr(&P->ctl->error, (uint32_t)ERR_DEPTH);
-      return;
-    }
+    u64 klo, khi;
+    child_bounds(sg, c, &klo, &khi);
     int flag = 0;
-    const U piv = cta_select_pivot_fast<C>(reinterpret_cast<const U *>(P->keys[db]),
-                                           !P->raw[db], cb, cl, P->dran, P->mitigation, xk, bc,
-                                           &flag);
+    u64 piv;
+    if ((int)depth > P->max_depth) {  // depth guard: bisect the key bound
+      piv = bisect_pivot(klo, khi);
+      if (threadIdx.x == 0) atomicAdd(&st[ST_BISECTED], 1ull);
+    } else {
+      piv = (u64)cta_select_pivot_fast<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
+                                          cb, cl, P->dran, P->mitigation, xk, bc, &flag);
+    }
     uint32_t kind = KIND_PARTITION;
     if (P->fast_paths)
       kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
-    cta_append_level<C, PAY>(P, nxt, cb, cb + cl, db, (u64)piv, kind, depth, 0, bc);
+    cta_append_level<C, PAY>(P, nxt, cb, cb + cl, db, piv, klo, khi, kind, depth, 0, bc);
   }
 }
 
@@ -694,7 +725,8 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
     u64 *dst[ST_COUNT] = {&ctl->stages, &ctl->sorted_bypass, &ctl->reversed_bypass,
                           &ctl->max_depth, &ctl->bytes_partition, &ctl->bytes_retire,
                           &ctl->writes0, &ctl->writes1, &ctl->verify_fallbacks,
-                          &ctl->partitioned_elements, &ctl->eq_runs, &ctl->eq_elements};
+                          &ctl->partitioned_elements, &ctl->eq_runs, &ctl->eq_elements,
+                          &ctl->bisected};
     if (threadIdx.x == ST_DEPTH) atomicMax(dst[ST_DEPTH], st[ST_DEPTH]);
     else atomicAdd(dst[threadIdx.x], st[threadIdx.x]);
   }
@@ -717,8 +749,16 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
         more = false;
       }
       if (ctl->error) more = false;
+      // drain the on-chip and run queues before a level could overflow them:
+      // one level appends at most 2 * seg_cap small segments and seg_cap runs
+      // (the large on-chip class cannot overflow: its segments are disjoint
+      // and longer than the small class's capacity, sq_cap[1] > n / that)
+      const uint32_t runs = (uint32_t)(ctl->run_packed >> 32);
+      const bool flush = more && (ctl->sq_count[0] + 2u * P->seg_cap > P->sq_cap[0] ||
+                                  runs + P->seg_cap > P->run_cap);
+      ctl->flush = flush ? 1u : 0u;
       __threadfence();
-      if (P->use_cond) cudaGraphSetConditional(P->cond, more ? 1u : 0u);
+      if (P->use_cond) cudaGraphSetConditional(P->cond, (more && !flush) ? 1u : 0u);
     }
   }
 }

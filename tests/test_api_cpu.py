@@ -48,7 +48,7 @@ def test_library_is_sm100a():
 
 def test_status_strings_and_abi():
     lib = N.lib()
-    assert lib.tsq_abi_version() == 1
+    assert lib.tsq_abi_version() == 2
     assert N.status_str(N.TSQ_ERR_BUSY) == "sorter instance is not reentrant"
     assert N.status_str(N.TSQ_OK) == "ok"
 
@@ -65,9 +65,13 @@ def test_workspace_bytes_scales():
 
 
 def test_abi_struct_sizes_match_header():
-    # tsq_params: 8 + 6*4 + 3*8 ; tsq_stats: 18 u64 + 2 floats
-    assert ctypes.sizeof(N.TsqParams) == 56
-    assert ctypes.sizeof(N.TsqStats) == 18 * 8 + 8
+    # tsq_params: 8 + 7*4 (+4 pad) + 2 pointers + 1*8 ; tsq_stats: 20 u64 + 2 floats;
+    # tsq_stage_record: 5*8 + 2*4 (static_asserts in tsq_capi.cu pin the C side)
+    assert ctypes.sizeof(N.TsqParams) == 64
+    assert ctypes.sizeof(N.TsqStats) == 20 * 8 + 8
+    assert ctypes.sizeof(N.TsqStageRecord) == 48
+    src = open(os.path.join(ROOT, "paper_1505_00558_b200", "csrc", "tsq_capi.cu")).read()
+    assert "sizeof(tsq_params) == 64" in src and "sizeof(tsq_stats) == 168" in src
 
 
 def test_sortconfig_validation_matches_reference():
@@ -87,7 +91,9 @@ def test_sortconfig_validation_matches_reference():
         T.GpuConfig(small_threshold=-1)
     assert T.GpuConfig().small_threshold == 0  # auto: the measured per-type default
     with pytest.raises(ValueError):
-        T.GpuConfig(max_depth=4)
+        T.GpuConfig(max_depth=1)
+    assert T.GpuConfig().max_depth == 0  # auto: max(24, 2 log2 n)
+    T.GpuConfig(max_depth=2)
 
 
 def test_rng_matches_reference_kats():

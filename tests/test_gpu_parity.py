@@ -332,11 +332,88 @@ def test_module_level_api(cuda_ok):
     T.free_temp_storage()
 
 
-def test_depth_guard_raises(cuda_ok):
-    x = np.random.default_rng(2).integers(0, 2**31, 1 << 22).astype(np.int32)
-    s = T.Sorter(seed=1, gpu=T.GpuConfig(max_depth=8))
-    with pytest.raises(T.DepthExceededError):
-        s.sort(_dev(x))
+@pytest.mark.parametrize("payload", [False, True])
+@pytest.mark.parametrize("dtype", [np.int32, np.uint64, np.float64])
+def test_depth_guard_bisects_key_bounds(cuda_ok, dtype, payload):
+    """Beyond GpuConfig.max_depth segments split at the midpoint of their key
+    bounds: the sort finishes bit-exact instead of raising (the reference's
+    _range always finishes, core.py:1643-1728)."""
+    rng = np.random.default_rng(2)
+    x = _random(dtype, 1 << 22, rng)
+    s = T.Sorter(seed=1, gpu=T.GpuConfig(max_depth=2))
+    d = _dev(x)
+    if payload:
+        p = _dev(np.arange(x.size, dtype=np.uint32))
+        st = s.sort_with_stats(T.Records(d, p))
+        assert_records_consistent(x, d.cpu().numpy(), p.cpu().numpy(), _oracle_sorted(x)[0])
+    else:
+        st = s.sort_with_stats(d)
+        assert d.cpu().numpy().tobytes() == _oracle_sorted(x)[0].tobytes()
+    assert st.gpu["bisected"] > 0 and st.gpu["error_flags"] == 0
+
+
+def test_sample_position_adversary(cuda_ok):
+    """The smallest keys placed at every position the root's pivot sampling
+    reads (any jitter), n = 2^24: no DepthExceededError, no TsqError,
+    bit-exact output."""
+    n = 1 << 24
+    rng = np.random.default_rng(9)
+    x = rng.permutation(n).astype(np.int32) + 4096
+    # the positions the root's 1023 strided samples read, jittered by the
+    # sorter's first dran exactly as the sampling kernel computes them
+    S = 1023
+    rng_m = T.MitigationRng(1)
+    rng_m.next()
+    step = (n - 1) / (S - 1)
+    shift = int(np.floor((rng_m.dran - 1.0) * step * 0.5))
+    i = np.arange(S)
+    pos = np.floor(i * step).astype(np.int64)
+    pos[-1] = n - 1
+    interior = (i != 0) & (i != S // 2) & (i != S - 1)
+    pos[interior] = np.clip(pos[interior] + shift, 0, n - 1)
+    hits = np.unique(pos)
+    x[hits] = np.arange(hits.size, dtype=np.int32) - hits.size
+    d = _dev(x)
+    st = T.Sorter(seed=1).sort_with_stats(d)
+    assert d.cpu().numpy().tobytes() == np.sort(x).tobytes()
+    assert st.gpu["error_flags"] == 0
+
+
+def test_queue_drain_rounds(cuda_ok, monkeypatch):
+    """With the smallest queues the flush rule allows, the level loop drains
+    the on-chip and run queues mid-recursion (outer graph loop) -- results
+    unchanged, no capacity error."""
+    monkeypatch.setenv("TSQ_DEBUG_MIN_QUEUES", "1")
+    rng = np.random.default_rng(12)
+    for hl in (False, True):
+        x = rng.integers(0, 5000, 1 << 21).astype(np.int32)
+        d = _dev(x)
+        s = T.Sorter(seed=1, gpu=T.GpuConfig(small_threshold=64, host_levels=hl))
+        st = s.sort_with_stats(d)
+        assert d.cpu().numpy().tobytes() == np.sort(x).tobytes()
+        assert st.gpu["flushes"] > 0 and st.gpu["error_flags"] == 0
+        k = rng.integers(0, 300, 1 << 20).astype(np.uint64)
+        dk, dp = _dev(k), _dev(np.arange(k.size, dtype=np.uint32))
+        st = s.sort_with_stats(T.Records(dk, dp))
+        assert_records_consistent(k, dk.cpu().numpy(), dp.cpu().numpy(), np.sort(k))
+        assert st.gpu["flushes"] > 0
+        s.free_temp_storage()
+
+
+def test_last_status_without_stats(cuda_ok):
+    """tsq_sort with stats == NULL returns without a sync;
+    tsq_workspace_last_status reports the outcome."""
+    import ctypes
+    from paper_1505_00558_b200 import _native as N
+    x = np.random.default_rng(3).integers(-2**31, 2**31, 1 << 20, dtype=np.int64).astype(np.int32)
+    d = _dev(x)
+    ws = N.Workspace(0)
+    stream = torch.cuda.current_stream().cuda_stream
+    st = N.lib().tsq_sort(ctypes.c_void_p(d.data_ptr()), None, d.numel(), N.TSQ_I32, N.TSQ_NONE,
+                          None, ws.handle, ctypes.c_void_p(stream), None)
+    assert st == N.TSQ_OK
+    assert N.lib().tsq_workspace_last_status(ws.handle, ctypes.c_void_p(stream)) == N.TSQ_OK
+    assert d.cpu().numpy().tobytes() == np.sort(x).tobytes()
 
 
 def test_sort_many_pipeline(cuda_ok):
