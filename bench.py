@@ -1,7 +1,7 @@
 """Benchmark: keys/s sorting int32 n = 2^26 on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--family uniform] [--n 67108864] [--families]
+                    [--family uniform] [--n 67108864] [--no-families]
 
 One step = one full three-way partition sort of n = 2^26 int32 keys (the
 BASELINE.json headline; generated like config 1 -- uniform over the full
@@ -21,10 +21,14 @@ Also reported on the same JSON line:
                keys of every partitioned segment) / partition-kernel time,
                against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline the CPU restatement of the reference (oracle/, C + OpenMP
-               tasks) on the box's host cores, on a bounded sample
+               tasks) on the box's host cores, on the same 2^26 workload
+  families     every BASELINE.json config at its own size: keys/s,
+               the partition-pass roofline from a host-driven run, the
+               oracle's CPU time on the same input, and a bit-exact check
+               against tests/golden/full.json
 --impl reference prints the reference arm's line: the same CPU restatement
-timed alone (the reference itself is pure Python and not installed on the
-GPU box).
+timed alone on the same workload (the reference itself is pure Python and
+not installed on the GPU box).
 """
 
 from __future__ import annotations
@@ -108,45 +112,97 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_baseline(n_sample: int, threads: int, family: str):
-    """The oracle (C restatement of the reference sort) on the host cores."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def full_golden():
+    """tests/golden/full.json: the oracle's hashes of every config at full size."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "full.json")) as f:
+            return {r["family"]: r for r in json.load(f)["data"]}
+    except OSError:
+        return {}
+
+
+def cpu_sort_time(keys, payload, threads: int):
+    """The oracle (C restatement of the reference sort) on the host cores:
+    seconds to sort a copy of keys (+ payload) in place."""
     from oracle import oracle as O
-    import workloads as W
-    keys, _ = W.generate(family, n_sample)
     x = keys.copy()
+    p = None if payload is None else payload.copy()
     t0 = time.perf_counter()
-    O.sort(x, seed=1, threads=threads)
+    O.sort(x, p, seed=1, threads=threads)
     dt = time.perf_counter() - t0
-    assert np.array_equal(x, np.sort(keys))
-    return n_sample / dt, dt
+    return dt, x
 
 
 def reference_arm(args, rank: int, world: int):
+    """The reference's CPU path on this box's host cores, on our arm's
+    workload (same generator, same n): the oracle port with all threads."""
     if rank != 0:
         return
+    import workloads as W
     threads = os.cpu_count() or 1
-    n_sample = 1 << args.sample_log2
-    vals = []
+    keys, _ = W.generate(args.family, args.n)
+    ms = []
+    ok = True
     for i in range(args.warmup + args.steps):
-        v, _ = cpu_baseline(n_sample, threads, args.family)
+        dt, out = cpu_sort_time(keys, None, threads)
+        if i == 0:
+            ok = out.tobytes() == np.sort(keys).tobytes()
         if i >= args.warmup:
-            vals.append(v)
-    value = statistics.median(vals)
+            ms.append(dt * 1e3)
+    ms_step = statistics.median(ms)
+    value = args.n / (ms_step / 1e3)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": n_sample / value * 1e3, "higher_is_better": True,
+        "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.family} int32 n=2^26 (bounded sample "
-                                f"n=2^{args.sample_log2} per step)",
-                   "n": args.n, "sample_n": n_sample},
+        "config": {"workload": f"{args.family} int32 n=2^{int(np.log2(args.n))} "
+                                "(C1 generator at the headline size)",
+                   "n": args.n, "same_config": True},
         "cpu_baseline": {"value": value, "unit": "keys/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.family} int32 n=2^{args.sample_log2} per step, "
-                                   f"oracle/ C restatement with {threads} OpenMP threads"},
+                         "cpu": cpu_model(),
+                         "sample": f"the full workload ({args.family} int32 n={args.n}) per "
+                                   f"step, oracle/ C restatement with {threads} OpenMP "
+                                   "threads; median step"},
         "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "sorted_ok": ok,
     }
     print(json.dumps(line), flush=True)
+
+
+def partition_roofline(T, sorter_args, run, peak, peak_kind):
+    """Roofline of the partition pass from a host-driven run (one event pair
+    per partition launch): algorithmic bytes (read every live key, write the
+    < and > keys; records add the payloads) / partition-kernel time."""
+    hl = T.Sorter(seed=1, gpu=T.GpuConfig(host_levels=True, **sorter_args))
+    run(hl)
+    trace = hl.last_level_trace or []
+    part_ms = sum(lv["ms"] for lv in trace)
+    part_bytes = sum(lv["bytes"] for lv in trace)
+    achieved = part_bytes / (part_ms / 1e3) / 1e9 if part_ms else 0.0
+    levels = [{"ms": round(lv["ms"], 4), "GBps": round(lv["bytes"] / lv["ms"] / 1e6, 1)
+               if lv["ms"] else 0.0, "segments": lv["segments"], "bytes": lv["bytes"]}
+              for lv in trace]
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "kernel": "partition_kernel",
+            "peak_kind": peak_kind, "launches": len(trace),
+            "bytes_per_launch_avg": part_bytes / max(1, len(trace)),
+            "ms_per_launch_avg": part_ms / max(1, len(trace)),
+            "min_level_frac": round(min((lv["bytes"] / lv["ms"] / 1e6 for lv in trace
+                                         if lv["ms"] > 0), default=0.0) / peak, 4),
+            "levels": levels}
 
 
 def our_arm(args, rank: int, world: int):
@@ -171,7 +227,6 @@ def our_arm(args, rank: int, world: int):
         work.copy_(src)
         sorter.sort(work)
     torch.cuda.synchronize()
-    ok = bool(torch.all(work[1:] >= work[:-1]).item())
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -186,6 +241,8 @@ def our_arm(args, rank: int, world: int):
             ends[i].record(stream)
         torch.cuda.synchronize()
     barrier()
+    # the last timed step's output: the sorted permutation of the input
+    ok = bool(torch.equal(work, torch.sort(src).values))
     # Device time of each step: the sort graph's own CUDA events, recorded on
     # the sorting stream before its first and after its last kernel
     # (stats.gpu["ms_total"]).  The outer events also enclose the host
@@ -202,31 +259,26 @@ def our_arm(args, rank: int, world: int):
     ms_step = ms_total / args.steps
     value = world * args.n / (ms_step / 1e3)
     g = stats[-1].gpu
-    # init + (partition, schedule) per level + 2 on-chip classes + retire
-    launches_per_step = 2 * int(g["levels"]) + 4
+    # init + (partition, schedule) per level + the drain round (2 on-chip
+    # classes, retire, drain) per flush and at the end + the control-block
+    # readback
+    launches_per_step = 1 + 2 * int(g["levels"]) + 4 * (1 + int(g["flushes"])) + 1
 
-    # roofline of the partition pass from a host-driven run (per-launch events)
-    hl = T.Sorter(seed=1, gpu=T.GpuConfig(host_levels=True))
-    work.copy_(src)
-    hl.sort(work)
-    trace = hl.last_level_trace or []
-    part_ms = sum(lv["ms"] for lv in trace)
-    part_bytes = sum(lv["bytes"] for lv in trace)
     peak, peak_kind = peaks()
-    achieved = part_bytes / (part_ms / 1e3) / 1e9 if part_ms else 0.0
-    traffic = None
+
+    def run_headline(s):
+        work.copy_(src)
+        s.sort(work)
+
+    roofline = partition_roofline(T, {}, run_headline, peak, peak_kind)
     tp = os.path.join(ROOT, "profiles", "partition_traffic.json")
+    roofline["traffic"] = None
     if os.path.exists(tp):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get("bytes_per_launch")
+                roofline["traffic"] = json.load(f).get("bytes_per_launch")
         except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "partition_kernel", "peak_kind": peak_kind,
-                "launches": len(trace), "bytes_per_launch_avg": part_bytes / max(1, len(trace)),
-                "ms_per_launch_avg": part_ms / max(1, len(trace))}
+            pass
 
     # end to end through the public API with pinned host buffers.  Headline
     # e2e: T.sort_many over K pinned host arrays -- every array's H2D and
@@ -250,7 +302,8 @@ def our_arm(args, rank: int, world: int):
     t0 = time.perf_counter()
     T.sort_many(hosts)
     e2e_ms_step = (time.perf_counter() - t0) * 1e3 / K
-    e2e_ok = all(bool(np.all(h.numpy()[1:] >= h.numpy()[:-1])) for h in hosts)
+    want = np.sort(keys)
+    e2e_ok = all(np.array_equal(h.numpy(), want) for h in hosts)
     single_ms = []
     for i in range(3):
         hosts[0].copy_(src_t)
@@ -258,7 +311,7 @@ def our_arm(args, rank: int, world: int):
         t0 = time.perf_counter()
         T.sort(hosts[0])                       # H2D, device sort, D2H, synchronous
         single_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_ok = e2e_ok and bool(np.all(hosts[0].numpy()[1:] >= hosts[0].numpy()[:-1]))
+    e2e_ok = e2e_ok and np.array_equal(hosts[0].numpy(), want)
     single_ms_call = statistics.median(single_ms)
     del hosts
     if world > 1:
@@ -267,16 +320,19 @@ def our_arm(args, rank: int, world: int):
         e2e_ms_step = float(t.item())
 
     cpu = None
+    threads = os.cpu_count() or 1
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        v, dt = cpu_baseline(1 << 24, threads, args.family)
-        cpu = {"value": v, "unit": "keys/s", "cores": threads, "kind": "port",
-               "sample": f"{args.family} int32 n=2^24, oracle/ C restatement, "
-                         f"{threads} OpenMP threads, {dt:.2f} s"}
+        dt, out = cpu_sort_time(keys, None, threads)
+        cpu = {"value": args.n / dt, "unit": "keys/s", "cores": threads, "kind": "port",
+               "cpu": cpu_model(),
+               "sample": f"the full workload ({args.family} int32 n={args.n}), oracle/ C "
+                         f"restatement with {threads} OpenMP threads, {dt:.2f} s",
+               "sorted_ok": out.tobytes() == want.tobytes()}
 
     fams = None
-    if args.families and rank == 0:
-        fams = family_table(T, W, torch)
+    if not args.no_families and rank == 0:
+        fams = family_table(T, W, torch, peak, peak_kind,
+                            cpu_threads=0 if (args.no_cpu or world > 1) else threads)
 
     if rank == 0:
         line = {
@@ -298,7 +354,8 @@ def our_arm(args, rank: int, world: int):
                     "ms_per_step": e2e_ms_step,
                     "mode": f"T.sort_many over {K} pinned host arrays (H2D/D2H of every "
                             "array timed, overlapped with neighbouring sorts)",
-                    "single_call_ms": single_ms_call},
+                    "single_call_ms": single_ms_call,
+                    "single_call_keys_per_s": args.n / (single_ms_call / 1e3)},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "sorted_ok": ok and e2e_ok,
@@ -310,8 +367,13 @@ def our_arm(args, rank: int, world: int):
         print(json.dumps(line), flush=True)
 
 
-def family_table(T, W, torch):
-    """Per input family at BASELINE.json sizes (device-resident, keys/s)."""
+def family_table(T, W, torch, peak, peak_kind, cpu_threads: int):
+    """Every BASELINE.json config at its own size (device-resident input):
+    keys/s (median of 3 timed sorts after a warm-up), the partition-pass
+    roofline of a host-driven run, the oracle's CPU time on the same input
+    with `cpu_threads` threads, and a bit-exact check of the GPU output
+    against tests/golden/full.json."""
+    gold = full_golden()
     out = {}
     s = T.Sorter(seed=1)
     for fam, n in W.FULL_N.items():
@@ -320,23 +382,40 @@ def family_table(T, W, torch):
         psrc = torch.from_numpy(pay).cuda() if pay is not None else None
         d = torch.empty_like(src)
         p = torch.empty_like(psrc) if psrc is not None else None
-        ms = []
-        for i in range(4):
+
+        def run(sorter):
             d.copy_(src)
             if p is not None:
                 p.copy_(psrc)
-            torch.cuda.synchronize()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record()
-            st = s.sort_with_stats(T.Records(d, p) if p is not None else d)
-            b.record()
-            torch.cuda.synchronize()
+            return sorter.sort_with_stats(T.Records(d, p) if p is not None else d)
+
+        ms = []
+        for i in range(4):
+            st = run(s)
             if i:
-                ms.append(a.elapsed_time(b))
+                ms.append(float(st.gpu["ms_total"]))
         m = statistics.median(ms)
-        out[fam] = {"n": n, "keys_per_s": n / (m / 1e3), "ms": m,
-                    "levels": int(st.gpu["levels"]), "depth": int(st.max_depth)}
+        got = d.cpu().numpy()
+        ok = fam in gold and W.sha16(got) == gold[fam]["sorted_sha"]
+        if p is not None:
+            po = p.cpu().numpy().astype(np.int64)
+            ok = ok and np.array_equal(keys[po], got) and \
+                np.array_equal(np.bincount(po, minlength=n), np.ones(n, np.int64))
+        rf = partition_roofline(T, {}, run, peak, peak_kind)
+        rf.pop("levels")
+        row = {"n": n, "dtype": str(keys.dtype) + ("+u32" if pay is not None else ""),
+               "keys_per_s": n / (m / 1e3), "ms": m, "levels": int(st.gpu["levels"]),
+               "depth": int(st.max_depth), "bit_exact_vs_oracle": bool(ok),
+               "roofline": {k: rf[k] for k in ("achieved", "frac", "min_level_frac",
+                                               "launches", "ms_per_launch_avg")}}
+        if cpu_threads:
+            dt, _ = cpu_sort_time(keys, pay, cpu_threads)
+            row["cpu"] = {"keys_per_s": n / dt, "s": round(dt, 3), "cores": cpu_threads,
+                          "kind": "port"}
+            row["gpu_over_cpu"] = round((n / (m / 1e3)) / (n / dt), 1)
+        out[fam] = row
+        del src, psrc, d, p
+        torch.cuda.empty_cache()
     return out
 
 
@@ -347,11 +426,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--family", default="uniform")
-    ap.add_argument("--n", type=int, default=1 << 26)
-    ap.add_argument("--families", action="store_true", help="add a per-family table")
+    ap.add_argument("--num-keys", "--n", dest="n", type=int, default=1 << 26)
+    ap.add_argument("--no-families", action="store_true",
+                    help="skip the per-config table (every BASELINE config at its size)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--sample-log2", type=int, default=24,
-                    help="reference arm: keys per timed CPU sample (2^k)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -1,35 +1,40 @@
 """BASELINE.json configs at full size on the GPU.
 
-Expected sorted-output hashes: C1 (2^20) and C2 (2^24) were produced by the
-Python reference itself (tests/golden/sorts.json, make_golden.py --full);
-the others are the SHA-256 prefixes of the sorted multisets recorded in
-SURVEY.md §8(d) (the ascending arrangement of a multiset of totally ordered
-keys is unique, and the reference produced identical bytes for C1, C2 and
-C3-ascending there).  Records additionally check the payload permutation.
+Expected sorted-output hashes come from tests/golden/full.json: the oracle
+(the C restatement pinned to the reference by tests/test_oracle.py) run
+once per config at full size by tests/golden/make_full.py.  C1 (2^20) and
+C2 (2^24) were also produced by the Python reference itself
+(tests/golden/sorts.json, make_golden.py --full) and agree.  Records
+additionally check the payload permutation.
 """
 
 from __future__ import annotations
+
+import json
+import os
 
 import numpy as np
 import pytest
 
 import paper_1505_00558_b200 as T
-from conftest import load_golden
+from conftest import GOLDEN, load_golden
 import workloads as W
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-SORTED_SHA = {
-    "uniform": "269fe819645bcf01", "few_distinct": "d2841550f77594f3",
-    "ascending": "dd35184592035e35", "descending": "dd35184592035e35",
-    "organ_pipe": "170074f3e9a74eb5", "nearly_sorted": "dd35184592035e35",
-    "stair": "6e1a45e386184cb9", "normal_f64": "8685af96a6b30d49",
-    "records": "8f4194de9c1db190",
-}
+with open(os.path.join(GOLDEN, "full.json")) as _f:
+    FULL = {r["family"]: r for r in json.load(_f)["data"]}
+SORTED_SHA = {fam: r["sorted_sha"] for fam, r in FULL.items()}
 
 
-def test_reference_full_hashes_agree_with_table():
+def test_full_golden_covers_every_config():
+    assert set(FULL) == set(W.FULL_N)
+    for fam, r in FULL.items():
+        assert r["n"] == W.FULL_N[fam]
+
+
+def test_reference_full_hashes_agree_with_oracle():
     for rec in load_golden("sorts.json"):
         if rec["n"] == W.FULL_N.get(rec["family"]):
             assert SORTED_SHA[rec["family"]] == rec["sorted_sha"]
@@ -39,6 +44,7 @@ def test_reference_full_hashes_agree_with_table():
 def test_full_size_family(cuda_ok, family):
     n = W.FULL_N[family]
     keys, payload = W.generate(family, n)
+    assert W.sha16(keys) == FULL[family]["input_sha"]
     s = T.Sorter(seed=1)
     dk = torch.from_numpy(keys).cuda()
     if payload is None:

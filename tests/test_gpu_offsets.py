@@ -62,9 +62,9 @@ def test_offset_view_records(cuda_ok, n, koff, poff):
     rng = np.random.default_rng(n + 7 * koff + poff)
     keys = rng.integers(0, 1 << 20, n + 8, dtype=np.uint64)
     kb = torch.from_numpy(keys).cuda()
-    pb = torch.from_numpy(np.arange(n + 8, dtype=np.uint32)).cuda()
+    # payload = index into the key view
+    pb = torch.from_numpy((np.arange(n + 8, dtype=np.int64) - poff).astype(np.uint32)).cuda()
     kv, pv = kb[koff:koff + n], pb[poff:poff + n]
-    pv.sub_(poff)  # payload = index into the key view
     T.Sorter(seed=1).sort(T.Records(kv, pv))
     k_in = keys[koff:koff + n]
     assert_records_consistent(k_in, kv.cpu().numpy(), pv.cpu().numpy(), _oracle(k_in))
