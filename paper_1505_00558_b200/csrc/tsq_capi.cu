@@ -41,7 +41,7 @@ int key_bytes_of(int dt);
 // outgrow the class.
 int default_small_t(int kt, int pt, size_t n) {
   const bool pay = pt == TSQ_U32;
-  if (key_bytes_of(kt) == 4) return pay || n <= (1u << 21) ? kSmallMax : kSmallHuge;
+  if (key_bytes_of(kt) == 4) return pay || n <= (1u << 21) ? kSmallMax : kSmallGiant;
   return kSmallMax;
 }
 
@@ -55,11 +55,22 @@ KernelSet make_set() {
   s.sched = reinterpret_cast<const void *>(&schedule_kernel<C, PAY>);
   s.small[0] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, kThreads>);
   s.small[1] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 2 * kThreads>);
-  s.small_smem[0] = SmallGeo<C, PAY, kThreads>::SMEM;
-  s.small_smem[1] = SmallGeo<C, PAY, 2 * kThreads>::SMEM;
+  s.small_smem[0] = RadixGeo<C, PAY, kThreads>::SMEM;
+  s.small_smem[1] = RadixGeo<C, PAY, 2 * kThreads>::SMEM;
   for (int c = 0; c < kSmallClasses; ++c) s.small_threads[c] = kThreads << c;
-  s.small_cap[0] = SmallGeo<C, PAY, kThreads>::CAP;
-  s.small_cap[1] = SmallGeo<C, PAY, 2 * kThreads>::CAP;
+  s.small_cap[0] = RadixGeo<C, PAY, kThreads>::CAP;
+  s.small_cap[1] = RadixGeo<C, PAY, 2 * kThreads>::CAP;
+  if constexpr (!PAY && sizeof(U) == 4) {
+    s.small[2] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 4 * kThreads>);
+    s.small_smem[2] = RadixGeo<C, PAY, 4 * kThreads>::SMEM;
+    s.small_cap[2] = RadixGeo<C, PAY, 4 * kThreads>::CAP;
+  } else {
+    // no 1024-thread class: nothing is queued past class 1's capacity
+    s.small[2] = nullptr;
+    s.small_smem[2] = 0;
+    s.small_threads[2] = 0;
+    s.small_cap[2] = s.small_cap[1];
+  }
   s.raw_order = C::kRawOrder;
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
@@ -139,6 +150,7 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = 0, bool staged = fals
   L.run_cap = 8u * L.seg_cap + 64u;
   L.sq_cap[0] = 2u * L.run_cap;
   L.sq_cap[1] = (uint32_t)(n / (size_t)(kSmallT + 1) + 2);
+  L.sq_cap[2] = (uint32_t)(n / (size_t)(kSmallHuge + 1) + 2);
   if (getenv("TSQ_DEBUG_MIN_QUEUES")) {
     // test knob: the smallest queues the flush rule allows, so the level
     // loop drains them every level or two (exercises the drain rounds)
@@ -247,12 +259,13 @@ int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem, int block = k
 }
 
 tsq_status prepare_small_smem(const KernelSet &ks) {
-  const void *fns[4] = {ks.part, ks.sched, ks.small[0], ks.small[1]};
-  const size_t sm[4] = {ks.part_smem, ks.sched_smem, ks.small_smem[0], ks.small_smem[1]};
+  const void *fns[2 + kSmallClasses] = {ks.part, ks.sched, ks.small[0], ks.small[1], ks.small[2]};
+  const size_t sm[2 + kSmallClasses] = {ks.part_smem, ks.sched_smem, ks.small_smem[0],
+                                        ks.small_smem[1], ks.small_smem[2]};
   // always opt in: dynamic + static shared memory may cross 48 KB even when
   // the dynamic part alone does not
-  for (int i = 0; i < 4; ++i)
-    TSQ_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+  for (int i = 0; i < 2 + kSmallClasses; ++i)
+    if (fns[i]) TSQ_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sm[i]));
   return TSQ_OK;
 }
@@ -285,6 +298,7 @@ cudaError_t launch_level(const KernelSet &ks, const LevelLaunch &L, Params **dst
 cudaError_t launch_drain(tsq_workspace *ws, const KernelSet &ks, Params **dst, cudaStream_t s) {
   void *args[1] = {dst};
   for (int c = 0; c < kSmallClasses; ++c) {
+    if (!ks.small[c]) continue;
     cudaError_t e = cudaLaunchKernel(
         ks.small[c], dim3(occupancy_grid(ws, ks.small[c], ks.small_smem[c], ks.small_threads[c])),
         dim3(ks.small_threads[c]), args, ks.small_smem[c], s);
@@ -335,6 +349,7 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
   p->small_t = kSmallHuge;
   p->sq_lim[0] = kSmallT;
   p->sq_lim[1] = kSmallHuge;
+  p->sq_lim[2] = kSmallGiant;
   p->reproducible = 0;
 }
 
@@ -415,26 +430,28 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   TSQ_CUDA(cudaGraphAddKernelNode(&schednode, body, &lnode, 1, &lk));
 
   cudaGraphNode_t tail[kSmallClasses + 1];
+  int ntail = 0;
   for (int c = 0; c < kSmallClasses; ++c) {
+    if (!ks.small[c]) continue;
     cudaKernelNodeParams sk = lk;
     sk.func = const_cast<void *>(ks.small[c]);
     sk.gridDim = dim3(occupancy_grid(ws, ks.small[c], ks.small_smem[c], ks.small_threads[c]));
     sk.blockDim = dim3(ks.small_threads[c]);
     sk.sharedMemBytes = (unsigned)ks.small_smem[c];
-    TSQ_CUDA(cudaGraphAddKernelNode(&tail[c], obody, &inode, 1, &sk));
+    TSQ_CUDA(cudaGraphAddKernelNode(&tail[ntail++], obody, &inode, 1, &sk));
   }
   cudaKernelNodeParams rk = lk;
   rk.func = const_cast<void *>(ks.retire);
   rk.gridDim = dim3(occupancy_grid(ws, ks.retire, 0));
   rk.sharedMemBytes = 0;
-  TSQ_CUDA(cudaGraphAddKernelNode(&tail[kSmallClasses], obody, &inode, 1, &rk));
+  TSQ_CUDA(cudaGraphAddKernelNode(&tail[ntail++], obody, &inode, 1, &rk));
   cudaKernelNodeParams dk = lk;
   dk.func = reinterpret_cast<void *>(&drain_kernel);
   dk.gridDim = dim3(1);
   dk.blockDim = dim3(32);
   dk.sharedMemBytes = 0;
   cudaGraphNode_t dnode;
-  TSQ_CUDA(cudaGraphAddKernelNode(&dnode, obody, tail, kSmallClasses + 1, &dk));
+  TSQ_CUDA(cudaGraphAddKernelNode(&dnode, obody, tail, ntail, &dk));
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e2, g, &onode, 1, ge->ev[2]));
   TSQ_CUDA(cudaGraphInstantiate(&ge->exec, g, 0));
   return TSQ_OK;
@@ -697,7 +714,7 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   small_t = TSQ_SMALL_T;
 #endif
   if (pp.small_threshold > 0)
-    small_t = pp.small_threshold < ks.small_cap[1] ? pp.small_threshold : ks.small_cap[1];
+    small_t = pp.small_threshold < ks.small_cap[2] ? pp.small_threshold : ks.small_cap[2];
   // stage export: host-driven levels, the sort in an internal copy, the
   // caller's buffers a view of each level's post-stage state
   const bool exporting = pp.stage_export != 0;

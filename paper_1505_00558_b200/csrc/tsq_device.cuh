@@ -23,7 +23,8 @@ constexpr int kThreads = 256;        // every kernel: 8 warps per CTA
 constexpr int kSmallT = 4096;        // on-chip sort, 256-thread class (<= this)
 constexpr int kSmallMax = 8192;      // on-chip sort, 512-thread class, 8-byte items
 constexpr int kSmallHuge = 16384;    // on-chip sort, 512-thread class, 4-byte keys only
-constexpr int kSmallClasses = 2;
+constexpr int kSmallGiant = 32768;   // on-chip sort, 1024-thread class, 4-byte keys only
+constexpr int kSmallClasses = 3;
 constexpr int kMaxSample = 1023;     // pivot sample size cap (2^10 - 1)
 constexpr int kRunChunk = 8192;      // elements per retire work item
 constexpr int kMaxLevels = 512;      // hard stop for the level loop (never reached: the
@@ -375,7 +376,7 @@ __device__ __forceinline__ u64 warp_sum64(u64 v) {
 
 // on-chip class of a segment of len keys
 __device__ __forceinline__ int small_class(const Params *P, long long len) {
-  return len <= P->sq_lim[0] ? 0 : 1;
+  return len <= P->sq_lim[0] ? 0 : (len <= P->sq_lim[1] ? 1 : 2);
 }
 
 // ---- pivot sample size: ~sqrt(len), 2^k - 1 with k in [5, 10] -------------

@@ -1,496 +1,375 @@
-// tsq_small.cuh -- on-chip sort of the segments the recursion leaves behind
-// (<= small_t keys): the role insertion_sort plays for ranges of at most
-// insertion_threshold keys in the reference (smallsort.py:12-47,
-// core.py:1652-1658), done as a bitonic sorting network.
+// tsq_small.cuh -- on-chip sort of a small segment: an LSD radix sort over
+// the segment's own key range.  This is the role insertion_sort plays in the
+// reference (smallsort.py:12-47) for ranges of <= insertion_threshold keys
+// (core.py:1652-1658); here, segments of <= small_t keys.
 //
-// One CTA (256 threads) per segment, padded to N = 256 * E keys (E = 1 .. 16
-// per thread) with +max sentinels.  Keys live in registers in blocked order
-// (thread t holds elements t*E .. t*E+E-1).  The network is the all-ascending
-// bitonic formulation: merge k starts with a "flip" stage (i against
-// i ^ (k-1)) followed by half-cleaners (i against i ^ j), and every
-// comparator puts the minimum at the lower index -- no direction logic, one
-// min/max pair per comparator.  Stages exchange data three ways:
-//   stride <  E      both keys in the thread's registers
-//   stride <  32 E   partner thread in the same warp (__shfl_xor_sync)
-//   stride >= 32 E   partner in another warp: one shared-memory round trip
-//                    in register-major order (conflict-free)
-// Global I/O is staged through shared memory (padded rows) so it coalesces.
-// Records sort (key, local index) pairs so equal keys keep their own payloads
-// and sentinels sort after every real key; payloads are gathered by index.
-// Output always lands in buffer 0.
+// By the time the recursion hands a segment to the on-chip sort, its keys lie
+// between two ancestor pivots, so their encoded range is narrow (uniform int32
+// at 2^26: ~20 bits for a 16K-key segment).  One CTA per segment:
+//
+//   1. coalesced load, encode, CTA-wide min / max; item = key - min (records:
+//      the local index packed below it while both fit, else in a second
+//      array); items go to shared memory and come back "blocked" (thread t
+//      holds positions t*KE .. t*KE + KE - 1, KE = ceil(len / NT));
+//   2. ceil(bits(range) / 5) stable counting passes of <= 5-bit digits, each:
+//        count  every thread bumps its own 16-bit counter (digit, thread) for
+//               each of its items, in position order;
+//        scan   one exclusive scan over the counters in (digit, thread) order
+//               gives every (digit, thread) its first output slot;
+//        rank   the same sweep again now hands out slots: each item goes to
+//               its slot in shared memory; the next pass reads them back
+//               blocked.
+//      Thread order = position order inside a digit, so every pass is stable
+//      and the LSD passes leave the items in key order.
+//   3. keys written back as min + item (caller's encoding); record payloads
+//      gathered by local index.
+//
+// No warp-collective ranking: __match_any_sync runs on the ADU pipe at ~2
+// SM-cycles per distinct digit in the warp and ballot-based peer masks take
+// ~9 instructions per digit bit (scripts/micro/match_tp.cu); a counter bump is
+// 6.  ~20 instructions per item per pass against ~300 per key for the
+// bitonic + merge-path sort this replaces (TSQ_ONCHIP_MERGE keeps that one
+// for comparison).
 #pragma once
+
+#include "tsq_bitonic.cuh"
 
 namespace tsq {
 
-template <typename U, bool PAY>
-struct SortItem {
-  U k;
-  uint32_t i;  // local index (records only)
-};
-
-template <typename U, bool PAY>
-__device__ __forceinline__ bool item_less(const SortItem<U, PAY> &a, const SortItem<U, PAY> &b) {
-  if (PAY) return a.k < b.k || (a.k == b.k && a.i < b.i);
-  return a.k < b.k;
-}
-
-// comparator: a <- min, b <- max
-template <typename U, bool PAY>
-__device__ __forceinline__ void cmpx(SortItem<U, PAY> &a, SortItem<U, PAY> &b) {
-  if (PAY) {
-    const bool sw = item_less<U, PAY>(b, a);
-    const SortItem<U, PAY> x = a;
-    a.k = sw ? b.k : a.k;
-    a.i = sw ? b.i : a.i;
-    b.k = sw ? x.k : b.k;
-    b.i = sw ? x.i : b.i;
-  } else {
-    const U x = a.k, y = b.k;
-    a.k = x < y ? x : y;
-    b.k = x < y ? y : x;
-  }
-}
-
-// x <- min(x, y) if keep_min else max(x, y)
-template <typename U, bool PAY>
-__device__ __forceinline__ void keep(SortItem<U, PAY> &x, const SortItem<U, PAY> &y,
-                                     bool keep_min) {
-  if (PAY) {
-    const bool take = item_less<U, PAY>(y, x) == keep_min;
-    x.k = take ? y.k : x.k;
-    x.i = take ? y.i : x.i;
-  } else {
-    const U mn = x.k < y.k ? x.k : y.k;
-    const U mx = x.k < y.k ? y.k : x.k;
-    x.k = keep_min ? mn : mx;
-  }
-}
-
 template <typename U>
-__device__ __forceinline__ U shfl_xor_u(U v, int m);
-template <>
-__device__ __forceinline__ uint32_t shfl_xor_u<uint32_t>(uint32_t v, int m) {
-  return __shfl_xor_sync(0xffffffffu, v, m);
-}
-template <>
-__device__ __forceinline__ u64 shfl_xor_u<u64>(u64 v, int m) {
-  return __shfl_xor_sync(0xffffffffu, v, m);
-}
-
-// Exchange with thread tid ^ m: y[r] = partner's v[rev ? E-1-r : r].
-template <typename U, bool PAY, int E>
-__device__ __forceinline__ void exchange(const SortItem<U, PAY> (&v)[E], SortItem<U, PAY> (&y)[E],
-                                         int m, bool rev, U *xk, uint32_t *xi) {
-  const int tid = threadIdx.x;
-  if (m < 32) {
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const SortItem<U, PAY> &s = rev ? v[E - 1 - r] : v[r];
-      y[r].k = shfl_xor_u<U>(s.k, m);
-      if (PAY) y[r].i = __shfl_xor_sync(0xffffffffu, s.i, m);
-    }
+__device__ __forceinline__ void warp_minmax(U &mn, U &mx) {
+  if constexpr (sizeof(U) == 4) {
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
   } else {
-    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-      xk[r * kThreads + tid] = v[r].k;
-      if (PAY) xi[r * kThreads + tid] = v[r].i;
-    }
-    __syncthreads();
-    const int p = tid ^ m;
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int rr = rev ? E - 1 - r : r;
-      y[r].k = xk[rr * kThreads + p];
-      if (PAY) y[r].i = xi[rr * kThreads + p];
+    for (int o = 16; o > 0; o >>= 1) {
+      const U a = __shfl_xor_sync(0xffffffffu, mn, o);
+      const U b = __shfl_xor_sync(0xffffffffu, mx, o);
+      mn = a < mn ? a : mn;
+      mx = b > mx ? b : mx;
     }
   }
 }
 
-// in-thread half-cleaners with strides E/2 .. 1 (compile-time indices)
-template <typename U, bool PAY, int E>
-__device__ __forceinline__ void half_clean_regs(SortItem<U, PAY> (&v)[E]) {
-#pragma unroll
-  for (int j = E / 2; j >= 1; j >>= 1) {
-#pragma unroll
-    for (int r = 0; r < E; ++r)
-      if (!(r & j)) cmpx<U, PAY>(v[r], v[r | j]);
-  }
-}
+// item slot i -> shared-memory word: one pad word per 32, so both the
+// striped (consecutive) and the blocked (stride KE) accesses spread over the
+// banks
+__device__ __forceinline__ int rpad(int i) { return i + (i >> 5); }
 
-// Bitonic sort of N = 256 * E items held as v[E] per thread (blocked).
-template <typename U, bool PAY, int E>
-__device__ __forceinline__ void block_bitonic(SortItem<U, PAY> (&v)[E], U *xk, uint32_t *xi) {
-  constexpr int N = kThreads * E;
-  const int tid = threadIdx.x;
-  // merges of size 2 .. E: entirely inside each thread
-#pragma unroll
-  for (int k = 2; k <= E; k <<= 1) {
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int p = r ^ (k - 1);
-      if (r < p) cmpx<U, PAY>(v[r], v[p]);
-    }
-#pragma unroll
-    for (int j = k >> 2; j >= 1; j >>= 1) {
-#pragma unroll
-      for (int r = 0; r < E; ++r)
-        if (!(r & j)) cmpx<U, PAY>(v[r], v[r | j]);
-    }
-  }
-  // merges of size 2E .. N: cross-thread strides first, then in registers
-#pragma unroll 1
-  for (int k = 2 * E; k <= N; k <<= 1) {
-    SortItem<U, PAY> y[E];
-    {
-      // flip: element (tid, r) against (tid ^ (k/E - 1), E-1-r)
-      const int m = k / E - 1;
-      const bool lower = (tid & (k / (2 * E))) == 0;
-      exchange<U, PAY, E>(v, y, m, true, xk, xi);
-#pragma unroll
-      for (int r = 0; r < E; ++r) keep<U, PAY>(v[r], y[r], lower);
-    }
-#pragma unroll 1
-    for (int j = k >> 2; j >= E; j >>= 1) {
-      const int m = j / E;
-      const bool lower = (tid & m) == 0;
-      exchange<U, PAY, E>(v, y, m, false, xk, xi);
-#pragma unroll
-      for (int r = 0; r < E; ++r) keep<U, PAY>(v[r], y[r], lower);
-    }
-    half_clean_regs<U, PAY, E>(v);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// The on-chip sort proper: every warp sorts 512 items (16 per lane) with a
-// bitonic network in registers and shuffles, then log2(len/512) rounds merge
-// pairs of sorted runs through shared memory along merge paths -- each
-// thread binary-searches where its 16 outputs start and merges them
-// sequentially.  Padding only to a multiple of 512 (merge runs are clamped to
-// the segment length).
-//
-// Sort item: keys only -> the key; records with 32-bit keys -> key << 32 |
-// local index in one u64; records with 64-bit keys -> (key, index) pairs in
-// two arrays.  The index breaks ties (every item distinct) and gathers the
-// payloads at the end.
-
-constexpr int kVT = 16;     // items per thread
-constexpr int kLogVT = 4;
-
-template <class C, bool PAY>
-struct MergeTraits {
-  typedef typename C::U U;
-  static constexpr bool kPack = PAY && sizeof(U) == 4;   // (key, index) in one u64
-  static constexpr bool kIdx = PAY && sizeof(U) == 8;    // separate index array
-  typedef typename std::conditional<kPack, u64, U>::type K;
+// Shared-memory geometry of one item form (T = u32 / u64 items, IDX =
+// separate 16-bit local-index array).  Counters: R (digit) rows of NT 16-bit
+// counters (see radix_cnt_byte for the layout), RMAX * NT * 2 bytes.
+template <int NT, int CAP, typename T, bool IDX>
+struct RadixForm {
+  static constexpr int CAPP = CAP + CAP / 32;              // padded item slots
+  static constexpr int DBMAX = (sizeof(T) == 8 && IDX) ? 4 : 5;
+  static constexpr int RMAX = 1 << DBMAX;
+  static constexpr size_t MISC = 512;                       // min/max exchange, warp totals
+  static constexpr size_t OFF_BUF = MISC;
+  static constexpr size_t OFF_IBUF = OFF_BUF + (size_t)CAPP * sizeof(T);
+  static constexpr size_t OFF_CNT = (OFF_IBUF + (IDX ? (size_t)CAPP * 2 : 0) + 15) & ~(size_t)15;
+  static constexpr size_t END = OFF_CNT + (size_t)RMAX * NT * 2;
 };
 
-__device__ __forceinline__ int pidx(int i) { return i + (i >> kLogVT); }  // padded rows
-
-template <typename K, bool IDX>
-__device__ __forceinline__ bool mless(K a, uint32_t ia, K b, uint32_t ib) {
-  return IDX ? (a < b || (a == b && ia < ib)) : a < b;
+// Counter (digit d, thread t) layout.  Threads form groups of 64, m = t / 64;
+// a row (digit) is NT/2 32-bit words, a group 32 of them: lane l = t % 32 of
+// the group's first warp owns the low half of one word, the same lane of its
+// second warp the high half.  So a warp's bumps touch 32 distinct words of
+// one block per row -- conflict-free whatever digits its lanes hold (rows are
+// a multiple of 32 words apart).  Inside a block the 16-byte chunks are
+// XOR-swizzled by m, so the scan threads (one per block) read their blocks
+// with conflict-free 16-byte vectors: lane l sits in chunk (l/4) ^ (m % 8).
+template <int NT>
+__device__ __forceinline__ uint32_t radix_cnt_byte(int t) {
+  const int m = t >> 6, h = (t >> 5) & 1, l = t & 31;
+  const int word = m * 32 + ((((l >> 2) ^ (m & 7)) << 2) | (l & 3));
+  return (uint32_t)(word * 4 + 2 * h);
 }
 
-template <typename K, bool IDX>
-__device__ __forceinline__ void mcmpx(K &a, uint32_t &ia, K &b, uint32_t &ib) {
-  if (IDX) {
-    const bool sw = mless<K, IDX>(b, ib, a, ia);
-    const K x = a; const uint32_t ix = ia;
-    a = sw ? b : a; ia = sw ? ib : ia;
-    b = sw ? x : b; ib = sw ? ix : ib;
-  } else {
-    const K x = a, y = b;
-    a = x < y ? x : y;
-    b = x < y ? y : x;
-  }
-}
-
-// in-register bitonic sort of kVT items (all-ascending formulation)
-template <typename K, bool IDX>
-__device__ __forceinline__ void sort_thread(K (&v)[kVT], uint32_t (&vi)[kVT]) {
-#pragma unroll
-  for (int k = 2; k <= kVT; k <<= 1) {
-#pragma unroll
-    for (int r = 0; r < kVT; ++r) {
-      const int p = r ^ (k - 1);
-      if (r < p) mcmpx<K, IDX>(v[r], vi[r], v[p], vi[p]);
-    }
-#pragma unroll
-    for (int j = k >> 2; j >= 1; j >>= 1) {
-#pragma unroll
-      for (int r = 0; r < kVT; ++r)
-        if (!(r & j)) mcmpx<K, IDX>(v[r], vi[r], v[r | j], vi[r | j]);
-    }
-  }
-}
-
-template <typename K>
-__device__ __forceinline__ K shfl_xor_k(K v, int m) {
-  return __shfl_xor_sync(0xffffffffu, v, m);
-}
-
-// x <- min(x, y) if keep_min else max(x, y)
-template <typename K, bool IDX>
-__device__ __forceinline__ void mkeep(K &x, uint32_t &ix, K y, uint32_t iy, bool keep_min) {
-  if (IDX) {
-    const bool take = mless<K, IDX>(y, iy, x, ix) == keep_min;
-    x = take ? y : x;
-    ix = take ? iy : ix;
-  } else {
-    const K mn = x < y ? x : y, mx = x < y ? y : x;
-    x = keep_min ? mn : mx;
-  }
-}
-
-// Bitonic sort of the warp's 32 * kVT items, lane l holding l*kVT ..
-// l*kVT + kVT - 1: in-thread merges first, then merges of 32 .. 32 kVT with
-// shuffle stages for the cross-lane strides.
-template <typename K, bool IDX>
-__device__ __forceinline__ void warp_sort(K (&v)[kVT], uint32_t (&vi)[kVT]) {
-  const int lane = threadIdx.x & 31;
-  sort_thread<K, IDX>(v, vi);
-#pragma unroll 1
-  for (int k = 2 * kVT; k <= 32 * kVT; k <<= 1) {
-    {
-      const int m = k / kVT - 1;
-      const bool lower = (lane & (k / (2 * kVT))) == 0;
-      K y[kVT];
-      uint32_t yi[kVT];
-#pragma unroll
-      for (int r = 0; r < kVT; ++r) {
-        y[r] = shfl_xor_k<K>(v[kVT - 1 - r], m);
-        yi[r] = IDX ? __shfl_xor_sync(0xffffffffu, vi[kVT - 1 - r], m) : 0u;
-      }
-#pragma unroll
-      for (int r = 0; r < kVT; ++r) mkeep<K, IDX>(v[r], vi[r], y[r], yi[r], lower);
-    }
-#pragma unroll 1
-    for (int j = k >> 2; j >= kVT; j >>= 1) {
-      const int m = j / kVT;
-      const bool lower = (lane & m) == 0;
-#pragma unroll
-      for (int r = 0; r < kVT; ++r) {
-        const K y = shfl_xor_k<K>(v[r], m);
-        const uint32_t yi = IDX ? __shfl_xor_sync(0xffffffffu, vi[r], m) : 0u;
-        mkeep<K, IDX>(v[r], vi[r], y, yi, lower);
-      }
-    }
-#pragma unroll
-    for (int j = kVT / 2; j >= 1; j >>= 1) {
-#pragma unroll
-      for (int r = 0; r < kVT; ++r)
-        if (!(r & j)) mcmpx<K, IDX>(v[r], vi[r], v[r | j], vi[r | j]);
-    }
-  }
-}
-
-// One merge step for the thread whose outputs start at `o`: runs of length R
-// (clamped to len) in (S, SI), kVT outputs into registers.
-template <typename K, bool IDX>
-__device__ __forceinline__ int merge_thread(const K *S, const uint32_t *SI, int o, int R, int len,
-                                            K (&out)[kVT], uint32_t (&oi)[kVT]) {
-  const int base = o & ~(2 * R - 1);
-  const int a0 = base, na = min(R, len - base);
-  const int b0 = base + na, nb = max(0, min(R, len - base - R));
-  const int diag = o - base;
-  int lo = max(0, diag - nb), hi = min(diag, na);
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    const int pa = pidx(a0 + mid), pb = pidx(b0 + diag - 1 - mid);
-    const K ka = S[pa], kb = S[pb];
-    const uint32_t ja = IDX ? SI[pa] : 0u, jb = IDX ? SI[pb] : 0u;
-    if (mless<K, IDX>(kb, jb, ka, ja)) hi = mid;
-    else lo = mid + 1;
-  }
-  int ia = a0 + lo, ib = b0 + (diag - lo);
-  const int ae = a0 + na, be = b0 + nb;
-  // an exhausted run reads as the sentinel (greater than every item)
-  const K SENT = ~K(0);
-  K ka = ia < ae ? S[pidx(ia)] : SENT, kb = ib < be ? S[pidx(ib)] : SENT;
-  uint32_t ja = IDX ? (ia < ae ? SI[pidx(ia)] : 0xffffffffu) : 0u;
-  uint32_t jb = IDX ? (ib < be ? SI[pidx(ib)] : 0xffffffffu) : 0u;
-  const int cnt = min(kVT, na + nb - diag);
-#pragma unroll
-  for (int r = 0; r < kVT; ++r) {
-    const bool ta = !mless<K, IDX>(kb, jb, ka, ja);
-    out[r] = ta ? ka : kb;
-    if (IDX) oi[r] = ta ? ja : jb;
-    const int nx = ta ? ++ia : ++ib;
-    const bool ok = nx < (ta ? ae : be);
-    const K kn = ok ? S[pidx(nx)] : SENT;
-    const uint32_t jn = IDX ? (ok ? SI[pidx(nx)] : 0xffffffffu) : 0u;
-    if (ta) { ka = kn; ja = jn; } else { kb = kn; jb = jn; }
-  }
-  return cnt;
-}
-
-// Class geometry.  MULT: 16-key output chunks per thread in a merge round
-// (the 512-thread class takes up to 16384 four-byte keys with two).
-// Single-buffer classes hold every merge round's outputs in registers and
-// write them back over the input after a barrier, so they need one padded
-// buffer instead of two -- that is what fits the two-chunk class and 8-byte
-// sort items into the 512-thread class's shared memory at 2 CTAs per SM.
 template <class C, bool PAY, int NT>
-struct SmallGeo {
-  typedef MergeTraits<C, PAY> M;
-  typedef typename M::K K;
-  static constexpr int CLASS = NT == kThreads ? 0 : 1;
-  static constexpr int MULT = (CLASS == 1 && !PAY && sizeof(typename C::U) == 4) ? 2 : 1;
-  static constexpr int CAP = NT * kVT * MULT;       // keys
-  static constexpr int NP = CAP + CAP / kVT;         // padded capacity (rows of kVT + 1)
-  static constexpr bool SINGLE =
-      NT == 2 * kThreads && (MULT > 1 || (sizeof(K) + (M::kIdx ? 4 : 0)) > 4);
-  static constexpr size_t SMEM = (SINGLE ? 1 : 2) * (size_t)NP * (sizeof(K) + (M::kIdx ? 4 : 0));
+struct RadixGeo {
+  typedef typename C::U U;
+  static constexpr int NW = NT / 32;
+  static constexpr int CLASS = NT == kThreads ? 0 : (NT == 2 * kThreads ? 1 : 2);
+  static constexpr int CAP = CLASS == 0   ? kSmallT
+                             : CLASS == 1 ? ((!PAY && sizeof(U) == 4) ? kSmallHuge : kSmallMax)
+                                          : kSmallGiant;
+  static_assert(CLASS < 2 || (!PAY && sizeof(U) == 4), "the 1024-thread class is 4-byte keys only");
+  static constexpr int KPT = CAP / NT;
+  static constexpr size_t S32 = RadixForm<NT, CAP, uint32_t, PAY>::END;
+  static constexpr size_t S64a = sizeof(U) == 8 ? RadixForm<NT, CAP, u64, PAY>::END : 0;
+  static constexpr size_t S64b = sizeof(U) == 8 ? RadixForm<NT, CAP, u64, false>::END : 0;
+  static constexpr size_t S64 = S64a > S64b ? S64a : S64b;
+  static constexpr size_t SMEM = S32 > S64 ? S32 : S64;
+  static_assert(KPT * NT == CAP, "capacity is a whole number of items per thread");
+  static_assert(2 * NW * sizeof(U) + 4 * NW <= RadixForm<NT, CAP, uint32_t, PAY>::MISC,
+                "misc region");
 };
 
-// Sort items: keys only -> the key; records with 32-bit keys -> key << 32 |
-// local index; records with 64-bit keys -> (key - lo) << 14 | local index
-// when the segment's keys span less than 2^50 (PK64: one u64 compare per
-// step, like the 32-bit case), else (key, index) pairs in two arrays.
-template <class C, bool PAY, int NT, bool PK64>
-__device__ __forceinline__ void small_sort_one(const Params *P, const SmallSeg &sm,
-                                               unsigned char *smem, u64 lo) {
+// Exclusive scan of the R x NT counters in (digit, thread) order.  In that
+// order a block (digit d, group m) is 64 consecutive counters: the 32 low
+// halves (threads 64m .. 64m+31) then the 32 high halves.  Scan thread g
+// takes block g = d * (NT/64) + m: the packed sum P of its 32 words is two
+// 16-bit totals (no carries: a segment has < 2^16 items), and with s0 = the
+// block's exclusive prefix, word j becomes (s0 | (s0 + lo(P)) << 16) plus the
+// packed running sum of the words before it.
+template <int NT>
+__device__ __forceinline__ void radix_scan(uint16_t *cnt, uint32_t *wt, int R) {
+  constexpr int NW = NT / 32;
+  constexpr int GPR = NT / 64;  // blocks per row
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool own = tid < R * GPR;
+  const int sw = (tid % GPR) & 7;
+  const uint4 *blk = reinterpret_cast<const uint4 *>(cnt) + tid * 8;
+  uint32_t packed = 0;
+  if (own) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 v = blk[c ^ sw];
+      packed += v.x + v.y + v.z + v.w;
+    }
+  }
+  const uint32_t sum = (packed & 0xffffu) + (packed >> 16);
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wt[warp] = inc;
+  __syncthreads();
+  uint32_t s0 = inc - sum;
+#pragma unroll
+  for (int i = 0; i < NW; ++i)
+    if (i < warp) s0 += wt[i];
+  if (own) {
+    uint32_t run = s0 | ((s0 + (packed & 0xffffu)) << 16);
+    uint4 *wb = reinterpret_cast<uint4 *>(cnt) + tid * 8;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      uint4 v = wb[c ^ sw];
+      uint4 o;
+      o.x = run; run += v.x;
+      o.y = run; run += v.y;
+      o.z = run; run += v.z;
+      o.w = run; run += v.w;
+      wb[c ^ sw] = o;
+    }
+  }
+}
+
+// Radix passes over items T whose digits occupy bits [b0, b0 + bits); IDX:
+// the local index travels in a 16-bit side array (else it is packed below
+// b0 for records, or absent).  On entry the encoded keys (U) sit in shared
+// memory at slot rpad(i) of a U-typed array over the same region; the first
+// pass turns them into items as it reads them.  `lo` is their minimum.
+template <class C, bool PAY, int NT, typename T, bool IDX>
+__device__ __forceinline__ void radix_run(const Params *P, const SmallSeg &sm,
+                                          unsigned char *smem, typename C::U lo, int b0,
+                                          int bits) {
   typedef typename C::U U;
-  typedef MergeTraits<C, PAY> M;
-  typedef typename M::K K;
-  typedef SmallGeo<C, PAY, NT> SG;
-  constexpr bool IDX = M::kIdx && !PK64;
-  constexpr bool PACK = M::kPack || PK64;   // (key, index) packed in one u64
-  constexpr int SH = M::kPack ? 32 : 14;    // index bits below the key
-  constexpr bool SINGLE = SG::SINGLE;
-  constexpr int NP = SG::NP;
-  constexpr int MULT = SG::MULT;
-  constexpr int LPT = kVT * MULT;  // keys per thread
-  // smem: buffers A, B [NP] of K | (records, 64-bit keys) index A, B [NP];
-  // single-buffer classes: A only
-  K *ka = reinterpret_cast<K *>(smem), *kb = SINGLE ? ka : ka + NP;  // current / other buffer
-  uint32_t *ia = reinterpret_cast<uint32_t *>(ka + (SINGLE ? NP : 2 * NP));
-  uint32_t *ib = SINGLE ? ia : ia + (IDX ? NP : 0);
+  typedef RadixGeo<C, PAY, NT> G;
+  typedef RadixForm<NT, G::CAP, T, IDX> F;
+  constexpr int KPT = G::KPT;
+  constexpr bool PACKED = PAY && !IDX;
   const int tid = threadIdx.x;
   const int len = sm.len;
-  // threads holding items: whole warps (the warp sort covers 32 * kVT)
-  const int rows = ((len + 32 * kVT - 1) / (32 * kVT)) * 32;
-  const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
-  const bool raw = P->raw[sm.buf] != 0;
-  // coalesced load into padded rows (sentinels complete the last rows): all
-  // of a thread's loads issued before any is used, so their latencies overlap
-  U raw_k[LPT];
-#pragma unroll
-  for (int q = 0; q < LPT; ++q) {
-    const int i = tid + q * NT;
-    raw_k[q] = i < len ? src[i] : U(0);
+  // active threads hold KPT consecutive positions each (t*KPT .. t*KPT +
+  // KPT - 1); pads past len (the last thread's tail) sort last (all ones)
+  const int NA = (len + KPT - 1) / KPT;
+  const bool act = tid < NA;
+  T *buf = reinterpret_cast<T *>(smem + F::OFF_BUF);
+  uint16_t *ibuf = reinterpret_cast<uint16_t *>(smem + F::OFF_IBUF);
+  uint16_t *cnt = reinterpret_cast<uint16_t *>(smem + F::OFF_CNT);
+  uint32_t *wt = reinterpret_cast<uint32_t *>(smem) + 64;
+  // this thread's counter of digit 0; rows are NT * 2 bytes apart
+  unsigned char *mycb = reinterpret_cast<unsigned char *>(cnt) + radix_cnt_byte<NT>(tid);
+  // this thread's slots: rpad(t*KPT + k) = rpad(t*KPT) + k (KPT divides 32)
+  T *mine = buf + rpad(tid * KPT);
+  uint16_t *imine = ibuf + rpad(tid * KPT);
+  const U *rmine = reinterpret_cast<const U *>(smem + F::OFF_BUF) + rpad(tid * KPT);
+  int passes = 0, db = 0;
+  if (bits > 0) {
+    passes = (bits + F::DBMAX - 1) / F::DBMAX;
+    db = (bits + passes - 1) / passes;
   }
-#pragma unroll
-  for (int q = 0; q < LPT; ++q) {
-    const int i = tid + q * NT;
-    if (i < rows * kVT) {
-      K x;
-      if (i < len) {
-        const U k = raw ? C::enc(raw_k[q]) : raw_k[q];
-        x = PACK ? (K)((((u64)k - lo) << SH) | (u64)i) : (K)k;
-      } else {
-        x = ~K(0);
-      }
-      ka[pidx(i)] = x;
-      if (IDX) ia[pidx(i)] = i < len ? (uint32_t)i : 0xffffffffu;
-    }
-  }
-  __syncthreads();
-  // every warp sorts runs of 32 rows (row = tid, tid + NT, ...: warp-uniform)
+  const uint32_t mask = (1u << db) - 1u;
+  const int R = 1 << db;
+  T it[KPT];
+  uint16_t ix[IDX ? KPT : 1];
 #pragma unroll 1
-  for (int row = tid; row < rows; row += NT) {
-    K v[kVT];
-    uint32_t vi[kVT];
+  for (int ps = 0; ps < passes; ++ps) {
+    const int sh = b0 + db * ps;
+    __syncthreads();   // previous scatter (or the key load) complete
+    if (ps == 0) {
+      if (act) {
 #pragma unroll
-    for (int r = 0; r < kVT; ++r) {
-      v[r] = ka[row * (kVT + 1) + r];
-      vi[r] = IDX ? ia[row * (kVT + 1) + r] : 0u;
-    }
-    warp_sort<K, IDX>(v, vi);
-#pragma unroll
-    for (int r = 0; r < kVT; ++r) {
-      ka[row * (kVT + 1) + r] = v[r];
-      if (IDX) ia[row * (kVT + 1) + r] = vi[r];
-    }
-  }
-  // merge rounds: output chunk m of a thread is row tid + m * NT
-  for (int R = 32 * kVT; R < len; R <<= 1) {
-    __syncthreads();
-    K out[MULT][kVT];
-    uint32_t oi[MULT][kVT];
-    int cnt[MULT];
-#pragma unroll
-    for (int m = 0; m < MULT; ++m) {
-      const int o = (tid + m * NT) * kVT;
-      cnt[m] = o < len ? merge_thread<K, IDX>(ka, ia, o, R, len, out[m], oi[m]) : 0;
-    }
-    if (SINGLE) __syncthreads();  // every thread has read its inputs
-#pragma unroll
-    for (int m = 0; m < MULT; ++m) {
-      const int row = tid + m * NT;
-#pragma unroll
-      for (int r = 0; r < kVT; ++r)
-        if (r < cnt[m]) {
-          kb[row * (kVT + 1) + r] = out[m][r];
-          if (IDX) ib[row * (kVT + 1) + r] = oi[m][r];
+        for (int k = 0; k < KPT; ++k) {
+          const int p = tid * KPT + k;
+          it[k] = p < len ? (((T)(rmine[k] - lo) << b0) | (PACKED ? (T)p : (T)0)) : ~T(0);
+          if (IDX) ix[k] = (uint16_t)p;
         }
+      }
+      // 64-bit keys in 32-bit items: the key array overlaps the counters
+      if (sizeof(U) > sizeof(T)) __syncthreads();
+    } else if (act) {
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        it[k] = mine[k];
+        if (IDX) ix[k] = imine[k];
+      }
     }
-    if (!SINGLE) {
-      K *tk = ka; ka = kb; kb = tk;
-      uint32_t *ti = ia; ia = ib; ib = ti;
+    {
+      uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+      const int n4 = R * NT / 8;
+      for (int i = tid; i < n4; i += NT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncthreads();
+    // count: this thread's items, in position order
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        uint16_t *a = reinterpret_cast<uint16_t *>(mycb + ((uint32_t)(it[k] >> sh) & mask) * (2 * NT));
+        *a = (uint16_t)(*a + 1u);
+      }
+    }
+    __syncthreads();
+    radix_scan<NT>(cnt, wt, R);
+    __syncthreads();
+    // rank + scatter, same order
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        uint16_t *a = reinterpret_cast<uint16_t *>(mycb + ((uint32_t)(it[k] >> sh) & mask) * (2 * NT));
+        const uint32_t r = *a;
+        *a = (uint16_t)(r + 1u);
+        buf[rpad((int)r)] = it[k];
+        if (IDX) ibuf[rpad((int)r)] = ix[k];
+      }
     }
   }
   __syncthreads();
+  // buf[0, len) holds the sorted items
   U *dst = reinterpret_cast<U *>(P->keys[0]) + sm.begin;
   const bool dst_raw = P->raw[0] != 0;
-  if (PAY && SINGLE) {
-    // payloads gathered by local index straight from the source (an L1/L2
-    // resident window) into registers, all before any is written (the
-    // source may be buffer 0 itself)
+  if (PAY) {
+    // payloads gathered by local index from the source (an L1/L2-resident
+    // window) into registers, all before any is written (the source may be
+    // buffer 0 itself)
     const uint32_t *ps = P->pay[sm.buf] + sm.begin;
-    uint32_t pv[LPT];
+    uint32_t pv[KPT];
 #pragma unroll
-    for (int q = 0; q < LPT; ++q) {
+    for (int q = 0; q < KPT; ++q) {
       const int i = tid + q * NT;
-      pv[q] = i < len ? ps[PACK ? (uint32_t)((u64)ka[pidx(i)] & ((1ull << SH) - 1)) : ia[pidx(i)]]
+      pv[q] = i < len ? ps[IDX ? (uint32_t)ibuf[rpad(i)]
+                               : (uint32_t)(buf[rpad(i)] & (T)((1u << b0) - 1u))]
                       : 0u;
     }
     __syncthreads();
     uint32_t *pd = P->pay[0] + sm.begin;
 #pragma unroll
-    for (int q = 0; q < LPT; ++q) {
+    for (int q = 0; q < KPT; ++q) {
       const int i = tid + q * NT;
       if (i < len) pd[i] = pv[q];
     }
-  } else if (PAY) {
-    // the same through the free merge buffer
-    const uint32_t *ps = P->pay[sm.buf] + sm.begin;
-    uint32_t *stage = reinterpret_cast<uint32_t *>(kb);
-    for (int i = tid; i < len; i += NT)
-      stage[i] = ps[PACK ? (uint32_t)((u64)ka[pidx(i)] & ((1ull << SH) - 1)) : ia[pidx(i)]];
-    __syncthreads();
-    uint32_t *pd = P->pay[0] + sm.begin;
-    for (int i = tid; i < len; i += NT) pd[i] = stage[i];
   }
-  for (int i = tid; i < len; i += NT) {
-    const K x = ka[pidx(i)];
-    const U k = PACK ? (U)(lo + ((u64)x >> SH)) : (U)x;
-    dst[i] = dst_raw ? C::dec(k) : k;
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int i = tid + q * NT;
+    if (i < len) {
+      const U k = lo + (U)(buf[rpad(i)] >> b0);
+      dst[i] = dst_raw ? C::dec(k) : k;
+    }
   }
 }
 
-// One CTA per queued segment (tickets).  NT = 256: the queue of segments of
-// <= kSmallT keys; NT = 512: kSmallT+1 .. the class capacity.
+// Sort one queued segment (all threads of the CTA).
 template <class C, bool PAY, int NT>
-__global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : (PAY ? 1 : 2))
+__device__ __forceinline__ void radix_sort_seg(const Params *P, const SmallSeg &sm,
+                                               unsigned char *smem) {
+  typedef typename C::U U;
+  typedef RadixGeo<C, PAY, NT> G;
+  constexpr int KPT = G::KPT, NW = G::NW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int len = sm.len;
+  const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
+  const bool raw = P->raw[sm.buf] != 0;
+  // coalesced load of the encoded keys into shared memory (slot rpad(i)),
+  // taking the min / max on the way
+  U *kbuf = reinterpret_cast<U *>(smem + RadixForm<NT, G::CAP, U, false>::OFF_BUF);
+  // (explicit global loads, all issued before the first shared store: a
+  // generic load could alias the shared array and would be serialised)
+  U mn = KeyMax<U>::v, mx = U(0);
+  constexpr int LB = (sizeof(U) == 8 || KPT < 16) ? 8 : 16;   // loads in flight per batch
+#pragma unroll
+  for (int q0 = 0; q0 < KPT; q0 += LB) {
+    U v[LB];
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int i = tid + (q0 + q) * NT;
+      v[q] = i < len ? ldcg(src + i) : U(0);
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int i = tid + (q0 + q) * NT;
+      if (i < len) {
+        const U x = raw ? C::enc(v[q]) : v[q];
+        kbuf[rpad(i)] = x;
+        mn = x < mn ? x : mn;
+        mx = x > mx ? x : mx;
+      }
+    }
+  }
+  warp_minmax<U>(mn, mx);
+  U *s_mm = reinterpret_cast<U *>(smem);
+  if (lane == 0) {
+    s_mm[warp] = mn;
+    s_mm[NW + warp] = mx;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const U a = s_mm[w], b = s_mm[NW + w];
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  const U range = mx - mn;
+  if (range == 0) {
+    // every key equal: already in order
+    U *dst = reinterpret_cast<U *>(P->keys[0]) + sm.begin;
+    const U k = P->raw[0] ? C::dec(mn) : mn;
+    if (PAY && sm.buf != 0) {
+      const uint32_t *ps = P->pay[sm.buf] + sm.begin;
+      uint32_t *pd = P->pay[0] + sm.begin;
+      for (int i = tid; i < len; i += NT) pd[i] = ps[i];
+    }
+    for (int i = tid; i < len; i += NT) dst[i] = k;
+    return;
+  }
+  const int bits = sizeof(U) == 4 ? 32 - __clz((uint32_t)range) : 64 - __clzll((long long)range);
+  // item form: 32-bit items whenever the range fits (records: index packed
+  // below the key offset while both fit in 32 bits), else 64-bit items
+  if (PAY && bits <= 18) {
+    radix_run<C, PAY, NT, uint32_t, false>(P, sm, smem, mn, 14, bits);
+  } else if (sizeof(U) == 4 || bits <= 32) {
+    radix_run<C, PAY, NT, uint32_t, PAY>(P, sm, smem, mn, 0, bits);
+  } else if constexpr (sizeof(U) == 8) {
+    if (PAY && bits <= 50) radix_run<C, PAY, NT, u64, false>(P, sm, smem, mn, 14, bits);
+    else radix_run<C, PAY, NT, u64, PAY>(P, sm, smem, mn, 0, bits);
+  }
+}
+
+// One CTA per queued segment (tickets), one kernel per class: NT = 256 takes
+// the queue of segments of <= kSmallT keys, NT = 512 kSmallT+1 .. its
+// capacity, NT = 1024 (4-byte keys only) the rest up to kSmallGiant.
+template <class C, bool PAY, int NT>
+__global__ void __launch_bounds__(NT, NT == kThreads ? 4 : (NT == 2 * kThreads ? 2 : 1))
     small_sort_kernel(const Params *__restrict__ P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
-  __shared__ u64 s_range[2];
   Ctl *ctl = P->ctl;
-  constexpr int cls = SmallGeo<C, PAY, NT>::CLASS;
+  constexpr int cls = RadixGeo<C, PAY, NT>::CLASS;
   const uint32_t n_q = ctl->sq_count[cls];
   const uint32_t cap = P->sq_cap[cls];
   const uint32_t count = n_q < cap ? n_q : cap;
@@ -504,30 +383,7 @@ __global__ void __launch_bounds__(NT, NT == kThreads ? (PAY ? 2 : 3) : (PAY ? 1 
     __syncthreads();
     if (t >= count) break;
     const SmallSeg sm = q[t];
-    if constexpr (MergeTraits<C, PAY>::kIdx) {
-      // 64-bit keys with payloads: the segment's key range decides the item
-      // form (one u64 when it spans < 2^50, else key + index arrays)
-      typedef typename C::U U;
-      const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
-      const bool raw = P->raw[sm.buf] != 0;
-      u64 mn = ~0ull, mx = 0ull;
-      for (int i = threadIdx.x; i < sm.len; i += NT) {
-        const u64 k = (u64)(raw ? C::enc(src[i]) : src[i]);
-        mn = k < mn ? k : mn;
-        mx = k > mx ? k : mx;
-      }
-      if (threadIdx.x == 0) { s_range[0] = ~0ull; s_range[1] = 0ull; }
-      __syncthreads();
-      atomicMin(&s_range[0], mn);
-      atomicMax(&s_range[1], mx);
-      __syncthreads();
-      const u64 lo = s_range[0], hi = s_range[1];
-      __syncthreads();
-      if (((hi - lo) >> 50) == 0) small_sort_one<C, PAY, NT, true>(P, sm, smem_raw, lo);
-      else small_sort_one<C, PAY, NT, false>(P, sm, smem_raw, 0ull);
-    } else {
-      small_sort_one<C, PAY, NT, false>(P, sm, smem_raw, 0ull);
-    }
+    radix_sort_seg<C, PAY, NT>(P, sm, smem_raw);
     elems += (uint64_t)sm.len;
     __syncthreads();
   }

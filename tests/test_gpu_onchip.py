@@ -1,8 +1,10 @@
 """GPU parity around the on-chip sort classes (tsq_small.cuh): segments of
-<= 4096 keys (256-thread class) and 4097 .. 8192 four-byte keys (512-thread
-class) finish in shared memory with warp bitonic networks + merge-path
-rounds.  Sizes straddle every class boundary and the partition pass's tile
-sizes; the inputs cover the shapes the reference battery exercises
+<= 4096 keys (256-thread class), 4097 .. 16384 four-byte keys / 8192 records
+and 8-byte keys (512-thread class) and 16385 .. 32768 four-byte keys
+(1024-thread class) finish in shared memory with an LSD radix sort over the
+segment's key range.  Sizes straddle every class boundary and the partition
+pass's tile sizes; key ranges straddle the radix digit and item-form
+boundaries; the inputs cover the shapes the reference battery exercises
 (datagen.py:106-198): uniform, few distinct, all equal, sorted, reversed,
 organ pipe, sawtooth, two sorted runs, and -0.0 / NaN for floats.  Bar:
 bit-exact against the CPU oracle (oracle/), the reference's algorithm
@@ -107,13 +109,60 @@ def test_onchip_whole_array_in_one_segment(sorter):
         assert st.gpu["levels"] == 0
 
 
+@pytest.mark.parametrize("n", [16383, 16384, 16385, 20000, 32767, 32768, 32769, 100000])
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.float32])
+def test_onchip_1024_thread_class(n, dtype, cuda_ok):
+    """The 1024-thread class (16385 .. 32768 four-byte keys): forced with
+    small_threshold=32768 at sizes around both of its boundaries."""
+    s = T.Sorter(seed=5, gpu=T.GpuConfig(small_threshold=32768))
+    rng = np.random.default_rng(n * 3 + 2)
+    for name, x in _shapes(n, rng, dtype).items():
+        _check(x, s)
+
+
+@pytest.mark.parametrize("bits", [1, 4, 5, 6, 10, 11, 15, 16, 17, 18, 19, 20, 21, 25, 26, 31, 32,
+                                  33, 40, 49, 50, 51, 63, 64])
+def test_onchip_key_range_bits(bits, cuda_ok):
+    """The radix sort runs ceil(bits / 5) digit passes over key - min, in
+    32-bit items while the range fits (records: with the index packed below
+    the key up to 18 bits), else 64-bit items (records: index packed up to
+    50 bits, else a side array).  Segments whose keys span exactly 2^bits
+    values (min and max present), for keys and records, 4- and 8-byte keys,
+    on-chip directly (n <= the cut) and after partition levels."""
+    from conftest import assert_records_consistent
+    rng = np.random.default_rng(bits)
+    for dt in (np.int32, np.uint32, np.int64, np.uint64):
+        nb = 8 * np.dtype(dt).itemsize
+        if bits > nb:
+            continue
+        ut = np.uint32 if nb == 32 else np.uint64
+        mask = (1 << bits) - 1
+        # keys built in the order-preserving unsigned encoding, then decoded
+        lo = int(rng.integers(0, (1 << nb) - mask, dtype=np.uint64)) if bits < nb else 0
+        for n in (777, 5000, 30000, 200000):
+            off = rng.integers(0, 1 << 63, n, dtype=np.uint64) * np.uint64(2) + \
+                rng.integers(0, 2, n, dtype=np.uint64)
+            off &= np.uint64(mask)
+            off[0], off[-1] = 0, mask
+            u = (np.uint64(lo) + off).astype(ut)
+            if np.dtype(dt).kind == "i":
+                u ^= ut(1 << (nb - 1))
+            keys = u.view(dt)
+            rng.shuffle(keys)
+            _check(keys, T.Sorter(seed=1))
+            pay = np.arange(n, dtype=np.uint32)
+            dk, dp = torch.from_numpy(keys.copy()).cuda(), torch.from_numpy(pay).cuda()
+            T.Sorter(seed=1).sort(T.Records(dk, dp))
+            assert_records_consistent(keys, dk.cpu().numpy(), dp.cpu().numpy(), np.sort(keys))
+
+
 @pytest.mark.parametrize("dtype", [np.int64, np.uint64, np.float64, np.int32, np.uint32])
 @pytest.mark.parametrize("n", [3000, 8192, 12000, 70001])
 def test_onchip_records_item_forms(sorter, dtype, n):
-    """Records: 64-bit keys sort as one packed u64 (key - segment min, index)
-    when a segment's keys span < 2^50, else as (key, index) pairs; full-range
-    keys, a narrow cluster and a mix of both exercise both forms (and the
-    32-bit keys' packed form).  Keys bit-exact, payload a permutation
+    """Records: items are key - segment min with the index packed below it
+    (32-bit items up to 18 bits of range, 64-bit items up to 50 bits), else
+    (key, index) pairs; full-range keys, a narrow cluster and a mix of both
+    exercise every form.  Keys bit-exact, payload a permutation
     consistent with the keys (BASELINE.json config 5)."""
     from conftest import assert_records_consistent
     rng = np.random.default_rng(n + 17)
