@@ -7,10 +7,10 @@
 // between two ancestor pivots, so their encoded range is narrow (uniform int32
 // at 2^26: ~20 bits for a 16K-key segment).  One CTA per segment:
 //
-//   1. coalesced load, encode, CTA-wide min / max; item = key - min (records:
-//      the local index packed below it while both fit, else in a second
-//      array); items go to shared memory and come back "blocked" (thread t
-//      holds positions t*KE .. t*KE + KE - 1, KE = ceil(len / NT));
+//   1. coalesced load into shared memory, encode, CTA-wide min / max; the
+//      active threads (ceil(len / KPT)) read KPT consecutive keys each back
+//      ("blocked") and form items = key - min (records: the local index
+//      packed below it while both fit, else in a 16-bit side array);
 //   2. ceil(bits(range) / 5) stable counting passes of <= 5-bit digits, each:
 //        count  every thread bumps its own 16-bit counter (digit, thread) for
 //               each of its items, in position order;
@@ -21,15 +21,20 @@
 //               blocked.
 //      Thread order = position order inside a digit, so every pass is stable
 //      and the LSD passes leave the items in key order.
-//   3. keys written back as min + item (caller's encoding); record payloads
-//      gathered by local index.
+//   3. keys written back as min + item (caller's encoding, coalesced);
+//      record payloads gathered by local index.
 //
-// No warp-collective ranking: __match_any_sync runs on the ADU pipe at ~2
-// SM-cycles per distinct digit in the warp and ballot-based peer masks take
-// ~9 instructions per digit bit (scripts/micro/match_tp.cu); a counter bump is
-// 6.  ~20 instructions per item per pass against ~300 per key for the
-// bitonic + merge-path sort this replaces (TSQ_ONCHIP_MERGE keeps that one
-// for comparison).
+// Measured alternatives (B200, uniform int32 2^26, profiles/r02*): warp-
+// collective ranking with __match_any_sync runs on the ADU pipe at ~2
+// SM-cycles per distinct digit in the warp (60 per 8-bit match,
+// scripts/micro/match_tp.cu) -- 2.3 ms for the on-chip sort; ballot-based
+// peer masks take ~9 instructions per digit bit; per-thread counters cost 6
+// instructions per bump.  Blocked global loads straight into registers
+// (no shared-memory transpose) were 1.6x slower (32 lines per load
+// instruction); two-at-a-time counter bumps cut the shared-memory latency
+// stalls but added 10 % instructions (net +4 %).  The round-1 warp bitonic +
+// merge-path sort took 0.95 ms at ~320 instructions per key; this one 0.68 ms
+// at ~176.
 #pragma once
 
 #include "tsq_bitonic.cuh"
@@ -163,7 +168,8 @@ __device__ __forceinline__ void radix_scan(uint16_t *cnt, uint32_t *wt, int R) {
 // the local index travels in a 16-bit side array (else it is packed below
 // b0 for records, or absent).  On entry the encoded keys (U) sit in shared
 // memory at slot rpad(i) of a U-typed array over the same region; the first
-// pass turns them into items as it reads them.  `lo` is their minimum.
+// pass turns them into items as it reads them back blocked.  `lo` is their
+// minimum.
 template <class C, bool PAY, int NT, typename T, bool IDX>
 __device__ __forceinline__ void radix_run(const Params *P, const SmallSeg &sm,
                                           unsigned char *smem, typename C::U lo, int b0,
@@ -188,14 +194,11 @@ __device__ __forceinline__ void radix_run(const Params *P, const SmallSeg &sm,
   // this thread's slots: rpad(t*KPT + k) = rpad(t*KPT) + k (KPT divides 32)
   T *mine = buf + rpad(tid * KPT);
   uint16_t *imine = ibuf + rpad(tid * KPT);
-  const U *rmine = reinterpret_cast<const U *>(smem + F::OFF_BUF) + rpad(tid * KPT);
-  int passes = 0, db = 0;
-  if (bits > 0) {
-    passes = (bits + F::DBMAX - 1) / F::DBMAX;
-    db = (bits + passes - 1) / passes;
-  }
+  const int passes = (bits + F::DBMAX - 1) / F::DBMAX;   // bits >= 1
+  const int db = (bits + passes - 1) / passes;
   const uint32_t mask = (1u << db) - 1u;
   const int R = 1 << db;
+  const U *rmine = reinterpret_cast<const U *>(smem + F::OFF_BUF) + rpad(tid * KPT);
   T it[KPT];
   uint16_t ix[IDX ? KPT : 1];
 #pragma unroll 1
@@ -296,10 +299,10 @@ __device__ __forceinline__ void radix_sort_seg(const Params *P, const SmallSeg &
   const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
   const bool raw = P->raw[sm.buf] != 0;
   // coalesced load of the encoded keys into shared memory (slot rpad(i)),
-  // taking the min / max on the way
+  // taking the min / max on the way (explicit global loads, a batch in
+  // flight before the first shared store: a generic load could alias the
+  // shared array and would be serialised)
   U *kbuf = reinterpret_cast<U *>(smem + RadixForm<NT, G::CAP, U, false>::OFF_BUF);
-  // (explicit global loads, all issued before the first shared store: a
-  // generic load could alias the shared array and would be serialised)
   U mn = KeyMax<U>::v, mx = U(0);
   constexpr int LB = (sizeof(U) == 8 || KPT < 16) ? 8 : 16;   // loads in flight per batch
 #pragma unroll
