@@ -33,15 +33,17 @@ struct KernelSet {
 
 int key_bytes_of(int dt);
 
-// Default on-chip cut (measured on B200, scripts/variants.py and
-// scripts/thr_sweep.py): 4-byte keys the two-chunk 512-thread class's 16384
-// (8192 up to 2^21 keys, where fewer, larger segments would leave SMs idle;
-// records 8192), 8-byte keys and records 8192 -- an on-chip merge round
-// costs less than the partition level it replaces until the sort items
-// outgrow the class.
+// Default on-chip cut (measured on B200, scripts/cut_sweep.py, profiles/r02*):
+// 4-byte keys 32768 above 2^21 keys (uniform int32 2^26: 2.03 ms at 32768,
+// 2.04 at 16384, 2.20 at 12288; 2^24: 0.66 / 0.70 / 0.76 ms) -- a radix
+// pass over one more key bit costs less than the partition level it saves;
+// 8192 up to 2^21 keys, where fewer, larger segments would leave SMs idle.
+// Records and 8-byte keys 8192: their 1024-thread class runs at one CTA per
+// SM and f64 segments need ~9 digit passes (normal f64 2^26: 4.85 ms at
+// 8192, 4.98 at 16384; records 2^27: 9.79 / 9.90 ms).
 int default_small_t(int kt, int pt, size_t n) {
   const bool pay = pt == TSQ_U32;
-  if (key_bytes_of(kt) == 4) return pay || n <= (1u << 21) ? kSmallMax : kSmallGiant;
+  if (key_bytes_of(kt) == 4 && !pay) return n <= (1u << 21) ? kSmallMax : kSmallGiant;
   return kSmallMax;
 }
 
@@ -60,17 +62,9 @@ KernelSet make_set() {
   for (int c = 0; c < kSmallClasses; ++c) s.small_threads[c] = kThreads << c;
   s.small_cap[0] = RadixGeo<C, PAY, kThreads>::CAP;
   s.small_cap[1] = RadixGeo<C, PAY, 2 * kThreads>::CAP;
-  if constexpr (!PAY && sizeof(U) == 4) {
-    s.small[2] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 4 * kThreads>);
-    s.small_smem[2] = RadixGeo<C, PAY, 4 * kThreads>::SMEM;
-    s.small_cap[2] = RadixGeo<C, PAY, 4 * kThreads>::CAP;
-  } else {
-    // no 1024-thread class: nothing is queued past class 1's capacity
-    s.small[2] = nullptr;
-    s.small_smem[2] = 0;
-    s.small_threads[2] = 0;
-    s.small_cap[2] = s.small_cap[1];
-  }
+  s.small[2] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 4 * kThreads>);
+  s.small_smem[2] = RadixGeo<C, PAY, 4 * kThreads>::SMEM;
+  s.small_cap[2] = RadixGeo<C, PAY, 4 * kThreads>::CAP;
   s.raw_order = C::kRawOrder;
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
@@ -150,7 +144,7 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = 0, bool staged = fals
   L.run_cap = 8u * L.seg_cap + 64u;
   L.sq_cap[0] = 2u * L.run_cap;
   L.sq_cap[1] = (uint32_t)(n / (size_t)(kSmallT + 1) + 2);
-  L.sq_cap[2] = (uint32_t)(n / (size_t)(kSmallHuge + 1) + 2);
+  L.sq_cap[2] = (uint32_t)(n / (size_t)(kSmallMax + 1) + 2);
   if (getenv("TSQ_DEBUG_MIN_QUEUES")) {
     // test knob: the smallest queues the flush rule allows, so the level
     // loop drains them every level or two (exercises the drain rounds)
@@ -349,7 +343,7 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
   p->small_t = kSmallHuge;
   p->sq_lim[0] = kSmallT;
   p->sq_lim[1] = kSmallHuge;
-  p->sq_lim[2] = kSmallGiant;
+  p->sq_lim[2] = kSmallHuge;
   p->reproducible = 0;
 }
 

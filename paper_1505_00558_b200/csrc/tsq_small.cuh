@@ -70,7 +70,7 @@ struct RadixForm {
   static constexpr int CAPP = CAP + CAP / 32;              // padded item slots
   static constexpr int DBMAX = (sizeof(T) == 8 && IDX) ? 4 : 5;
   static constexpr int RMAX = 1 << DBMAX;
-  static constexpr size_t MISC = 512;                       // min/max exchange, warp totals
+  static constexpr size_t MISC = 1024;  // min/max exchange [0, 512), warp totals [512, 640)
   static constexpr size_t OFF_BUF = MISC;
   static constexpr size_t OFF_IBUF = OFF_BUF + (size_t)CAPP * sizeof(T);
   static constexpr size_t OFF_CNT = (OFF_IBUF + (IDX ? (size_t)CAPP * 2 : 0) + 15) & ~(size_t)15;
@@ -99,8 +99,7 @@ struct RadixGeo {
   static constexpr int CLASS = NT == kThreads ? 0 : (NT == 2 * kThreads ? 1 : 2);
   static constexpr int CAP = CLASS == 0   ? kSmallT
                              : CLASS == 1 ? ((!PAY && sizeof(U) == 4) ? kSmallHuge : kSmallMax)
-                                          : kSmallGiant;
-  static_assert(CLASS < 2 || (!PAY && sizeof(U) == 4), "the 1024-thread class is 4-byte keys only");
+                                          : ((!PAY && sizeof(U) == 4) ? kSmallGiant : kSmallHuge);
   static constexpr int KPT = CAP / NT;
   static constexpr size_t S32 = RadixForm<NT, CAP, uint32_t, PAY>::END;
   static constexpr size_t S64a = sizeof(U) == 8 ? RadixForm<NT, CAP, u64, PAY>::END : 0;
@@ -108,8 +107,7 @@ struct RadixGeo {
   static constexpr size_t S64 = S64a > S64b ? S64a : S64b;
   static constexpr size_t SMEM = S32 > S64 ? S32 : S64;
   static_assert(KPT * NT == CAP, "capacity is a whole number of items per thread");
-  static_assert(2 * NW * sizeof(U) + 4 * NW <= RadixForm<NT, CAP, uint32_t, PAY>::MISC,
-                "misc region");
+  static_assert(2 * NW * sizeof(U) <= 512 && NW <= 32, "misc region");
 };
 
 // Exclusive scan of the R x NT counters in (digit, thread) order.  In that
@@ -188,7 +186,7 @@ __device__ __forceinline__ void radix_run(const Params *P, const SmallSeg &sm,
   T *buf = reinterpret_cast<T *>(smem + F::OFF_BUF);
   uint16_t *ibuf = reinterpret_cast<uint16_t *>(smem + F::OFF_IBUF);
   uint16_t *cnt = reinterpret_cast<uint16_t *>(smem + F::OFF_CNT);
-  uint32_t *wt = reinterpret_cast<uint32_t *>(smem) + 64;
+  uint32_t *wt = reinterpret_cast<uint32_t *>(smem) + 128;
   // this thread's counter of digit 0; rows are NT * 2 bytes apart
   unsigned char *mycb = reinterpret_cast<unsigned char *>(cnt) + radix_cnt_byte<NT>(tid);
   // this thread's slots: rpad(t*KPT + k) = rpad(t*KPT) + k (KPT divides 32)

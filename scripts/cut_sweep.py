@@ -1,25 +1,39 @@
-"""Device time of uniform int32 2^26 sorts at several on-chip cuts (dev tool)."""
+"""Device time of full-size sorts at several on-chip cuts (dev tool):
+    python scripts/cut_sweep.py uniform:67108864 normal_f64:67108864 records:134217728"""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
 import torch
 
 import paper_1505_00558_b200 as T
 import workloads as W
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 26
-keys, _ = W.generate("uniform", n)
-src = torch.from_numpy(keys).cuda()
-d = torch.empty_like(src)
-for cut in (8192, 12288, 16384, 24576, 32768):
-    s = T.Sorter(seed=1, gpu=T.GpuConfig(small_threshold=cut))
-    ms = []
-    for i in range(6):
-        d.copy_(src)
-        st = s.sort_with_stats(d)
-        if i:
-            ms.append(st.gpu["ms_total"])
-    ms.sort()
-    ok = torch.equal(d, torch.sort(src).values)
-    print(f"n=2^{n.bit_length() - 1} cut {cut:6d}: {ms[len(ms) // 2]:.3f} ms  levels {st.gpu['levels']}  ok={ok}", flush=True)
+specs = sys.argv[1:] or ["uniform:67108864"]
+for spec in specs:
+    cuts = (8192, 12288, 16384) if spec.startswith('records') else (8192, 12288, 16384, 24576, 32768)
+    fam, n = spec.split(":")
+    n = int(n)
+    keys, pay = W.generate(fam, n)
+    src = torch.from_numpy(keys).cuda()
+    d = torch.empty_like(src)
+    psrc = torch.from_numpy(pay).cuda() if pay is not None else None
+    p = torch.empty_like(psrc) if psrc is not None else None
+    want = np.sort(keys)
+    for cut in cuts:
+        s = T.Sorter(seed=1, gpu=T.GpuConfig(small_threshold=cut))
+        ms = []
+        for i in range(5):
+            d.copy_(src)
+            if p is not None:
+                p.copy_(psrc)
+            st = s.sort_with_stats(T.Records(d, p) if p is not None else d)
+            if i:
+                ms.append(st.gpu["ms_total"])
+        ms.sort()
+        ok = bool(np.array_equal(d.cpu().numpy(), want))
+        print(f"{fam} n=2^{n.bit_length() - 1} cut {cut:6d}: {ms[len(ms) // 2]:.3f} ms  "
+              f"levels {st.gpu['levels']}  ok={ok}", flush=True)
+        del s
+        torch.cuda.empty_cache()
