@@ -22,7 +22,8 @@
 //                      CTA advances the level and sets the CUDA-graph loop
 //                      condition
 //   small_sort_kernel  on-chip sort of segments <= small_t (insertion_sort's
-//                      role, smallsort.py:12-47): warp bitonic + merge path
+//                      role, smallsort.py:12-47): LSD radix sort over the
+//                      segment's key range
 //   retire_kernel      writes ==p runs and verified runs into buffer 0
 //
 // Buffers: keys[0] is the caller's array (raw encoding), keys[1] the
@@ -172,8 +173,8 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
 __global__ void drain_kernel(const Params *__restrict__ P) {
   Ctl *ctl = P->ctl;
   if (threadIdx.x != 0) return;
-  ctl->small_segs_done += (u64)ctl->sq_count[0] + (u64)ctl->sq_count[1];
   for (int c = 0; c < kSmallClasses; ++c) {
+    ctl->small_segs_done += (u64)ctl->sq_count[c];
     ctl->sq_count[c] = 0;
     ctl->sq_ticket[c] = 0;
   }
