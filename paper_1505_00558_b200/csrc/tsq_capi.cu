@@ -826,12 +826,15 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
               (ws->h_ctl->dbg[1] - ws->h_ctl->dbg[0]) * 1e-3, (ws->h_ctl->dbg[2] - ws->h_ctl->dbg[1]) * 1e-3,
               (ws->h_ctl->dbg[3] - ws->h_ctl->dbg[2]) * 1e-3);
     if (getenv("TSQ_DEBUG_LEVELS"))
-      fprintf(stderr, "   cta task ns: head %llu pivot %llu append %llu\n",
+      fprintf(stderr, "   cta task / sched ns: head|tasks %llu pivot|end %llu append %llu\n",
               ws->h_ctl->dbg[5] >> 40, (ws->h_ctl->dbg[5] >> 20) & 0xfffff, ws->h_ctl->dbg[5] & 0xfffff);
+    if (getenv("TSQ_DEBUG_LEVELS"))
+      fprintf(stderr, "   warp round ns: tasks %llu claims+writes %llu | sched loop %llu end %llu\n",
+              ws->h_ctl->dbg[4] >> 32, ws->h_ctl->dbg[4] & 0xffffffffull,
+              ws->h_ctl->dbg[7] >> 32, ws->h_ctl->dbg[7] & 0xffffffffull);
     if (getenv("TSQ_DEBUG_LEVELS")) {  // reset the phase timers for the next level
-      TSQ_CUDA(cudaMemsetAsync(&ws->d_ctl->dbg[0], 0, 6 * sizeof(u64), s));
+      TSQ_CUDA(cudaMemsetAsync(&ws->d_ctl->dbg[0], 0, 8 * sizeof(u64), s));
       TSQ_CUDA(cudaMemsetAsync(&ws->d_ctl->dbg[0], 0xff, sizeof(u64), s));
-      TSQ_CUDA(cudaMemsetAsync(&ws->d_ctl->dbg[4], 0xff, sizeof(u64), s));
     }
     if (ws->h_ctl->cur_nseg == 0 || ws->h_ctl->error) break;
     const uint32_t nseg = ws->h_ctl->cur_nseg;

@@ -566,7 +566,6 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
     atomicMax(&ctl->dbg[1], tp0);   // last CTA done partitioning
     atomicMax(&ctl->dbg[2], tp1);   // barrier released
     atomicMax(&ctl->dbg[3], tp2);   // last schedule phase done
-    atomicMin(&ctl->dbg[4], tp1);
   }
 #endif
 }

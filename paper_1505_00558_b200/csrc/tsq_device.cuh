@@ -103,7 +103,7 @@ struct Ctl {
   u64 bisected;             // segments split at their key-bound midpoint
   uint32_t gbar;            // level kernel: CTAs through the partition phase
   uint32_t prev_nseg;       // segments of the level before `level` (stage export)
-  u64 dbg[6];               // experiment timers (TSQ_EXP_PHASE_CLOCK)
+  u64 dbg[8];               // experiment timers (TSQ_EXP_PHASE_CLOCK)
 };
 
 // Everything a kernel needs; lives in device memory, written by the init

@@ -55,10 +55,20 @@ __device__ __forceinline__ T bcast(T v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
 
-// Tiles are dealt round-robin: CTA b takes tiles b, b + G, b + 2G, ...  of
-// the level (G = persistent grid size), so processing order follows tile
-// order across CTAs (a look-back waits on its predecessors) and no claim
-// sits on the producer's critical path.
+// Tiles are claimed in "guided" chunks from the level's ticket: while many
+// remain a CTA takes up to 32 consecutive tiles at a time (their segments
+// resolved one lane each, so the dependent loads overlap), near the end
+// single tiles -- the pass ends within a tile or two on every CTA instead of
+// the ~12 us spread of a static round-robin deal.  Claims go out in
+// increasing tile order, so a look-back (reproducible mode) only ever waits
+// on tiles already claimed; the next chunk is claimed before the current one
+// runs out, so the claim's round trip stays off the producer's path.
+__device__ __forceinline__ uint32_t guided_chunk(uint32_t claimed, uint32_t ntiles, uint32_t grid) {
+  const uint32_t left = claimed < ntiles ? ntiles - claimed : 0u;
+  uint32_t c = left / (4u * grid);
+  return c < 1u ? 1u : (c > 32u ? 32u : c);
+}
+
 template <class C, bool PAY>
 __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t ntiles,
                                               typename C::U *in_k, uint32_t *in_p, u64 *full,
@@ -68,16 +78,33 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
   const int lane = threadIdx.x & 31;
   const uint32_t level = P->ctl->level;
   (void)level;
-  const u64 grid = gridDim.x;
-  TileSeg mine;  // lane j: the tile of iteration (it & ~31) + j
+  uint32_t *ticket = &P->ctl->tile_ticket;
+  const uint32_t grid = gridDim.x;
+  TileSeg mine;  // lane j: the tile c0 + j of the current chunk
+  // current chunk [c0, c0 + cn) at position ci; the next one, claimed ahead
+  uint32_t c0 = 0, cn = 0, ci = 0, n0 = 0, nn = 0;
+  if (lane == 0) {
+    nn = guided_chunk(0u, ntiles, grid);
+    n0 = atomicAdd(ticket, nn);
+  }
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % G::STAGES);
     const uint32_t j = it / G::STAGES;
-    const u64 t64 = blockIdx.x + (u64)it * grid;
-    if ((it & 31u) == 0) {
-      const u64 tl = blockIdx.x + (u64)(it + lane) * grid;
-      mine = resolve_tile(P, cur, tl < ntiles ? (uint32_t)tl : ntiles, ntiles);
+    if (ci == cn) {
+      // move to the claimed chunk; claim the one after it right away
+      c0 = __shfl_sync(0xffffffffu, n0, 0);
+      cn = __shfl_sync(0xffffffffu, nn, 0);
+      ci = 0;
+      if (lane == 0 && c0 < ntiles) {
+        nn = guided_chunk(c0 + cn, ntiles, grid);
+        n0 = atomicAdd(ticket, nn);
+      }
+      const uint32_t tl = c0 + (uint32_t)lane;
+      mine = resolve_tile(P, cur, (lane < (int)cn && tl < ntiles) ? tl : ntiles, ntiles);
     }
+    const u64 t64 = (u64)c0 + ci;
+    const int src_lane = (int)ci;
+    ++ci;
     if (j > 0) wait_empty_producer(&empty[s], (j - 1) & 1u);
     if (t64 >= ntiles) {
       // out of tiles: a DONE marker in the next stage stops every role.  The
@@ -98,7 +125,6 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
       return;
     }
     const uint32_t t = (uint32_t)t64;
-    const int src_lane = (int)(it & 31u);
     const long long begin = bcast(mine.begin, src_lane), end = bcast(mine.end, src_lane);
     const u64 pivot = bcast(mine.pivot, src_lane);
     const uint32_t sid = bcast(mine.sid, src_lane), tile_base = bcast(mine.tile_base, src_lane);

@@ -17,6 +17,14 @@
 
 namespace tsq {
 
+// experiment timers (TSQ_EXP_PHASE_CLOCK builds only)
+#ifdef TSQ_EXP_PHASE_CLOCK
+#define TSQ_TCLK(v) u64 v; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#else
+#define TSQ_TCLK(v) ((void)0)
+#endif
+
+
 // per-CTA statistics (shared-memory atomics, one global flush per CTA)
 enum SchedStat {
   ST_STAGES, ST_SORTED, ST_REVERSED, ST_DEPTH, ST_BYTES_PART, ST_BYTES_RETIRE, ST_W0, ST_W1,
@@ -392,6 +400,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     rs.run[warp].valid = 0;
   }
   __syncwarp();
+  TSQ_TCLK(w0);
   if (have) {
     const uint32_t sid = task >> 1;
     const int c = (int)(task & 1u);
@@ -461,19 +470,22 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
       }
     }
   }
+  TSQ_TCLK(w1);
   sched_sync();
-  // one claim per queue for the whole round
-  if (threadIdx.x == 0) {
-    uint32_t nl = 0, nt = 0, nr = 0, nc = 0, nq[kSmallClasses] = {};
+  // one claim per queue for the whole round, the queues' atomics issued by
+  // separate lanes of warp 0 so their round trips overlap
+  if (threadIdx.x < 2 + kSmallClasses) {
+    uint32_t nl = 0, nt = 0, nr = 0, nc = 0, nq = 0;
+    const int q = (int)threadIdx.x - 2;
     for (int w = 0; w < kThreads / 32; ++w) {
       for (int c = 0; c < 2; ++c) {
         if (rs.lv[w][c].valid) { ++nl; nt += rs.lv[w][c].ntiles; }
-        if (rs.sm[w][c].valid) ++nq[small_class(P, rs.sm[w][c].len)];
+        if (rs.sm[w][c].valid && q >= 0 && small_class(P, rs.sm[w][c].len) == q) ++nq;
       }
       if (rs.run[w].valid) { ++nr; nc += rs.run[w].nchunks; }
     }
     Ctl *ctl = P->ctl;
-    if (nl) {
+    if (threadIdx.x == 0 && nl) {
       const u64 old = atomicAdd(&ctl->next_packed, ((u64)nl << 32) | nt);
       rs.lv_slot0 = (uint32_t)(old >> 32);
       rs.lv_tile0 = (uint32_t)old;
@@ -481,8 +493,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
         rs.lv_slot0 = kDone;
       }
-    }
-    if (nr) {
+    } else if (threadIdx.x == 1 && nr) {
       const u64 old = atomicAdd(&ctl->run_packed, ((u64)nr << 32) | nc);
       rs.run_slot0 = (uint32_t)(old >> 32);
       rs.run_chunk0 = (uint32_t)old;
@@ -490,14 +501,11 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
         rs.run_slot0 = kDone;
       }
-    }
-    for (int q = 0; q < kSmallClasses; ++q) {
-      if (nq[q]) {
-        rs.sq_slot0[q] = atomicAdd(&ctl->sq_count[q], nq[q]);
-        if (rs.sq_slot0[q] + nq[q] > P->sq_cap[q]) {
-          atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
-          rs.sq_slot0[q] = kDone;
-        }
+    } else if (q >= 0 && nq) {
+      rs.sq_slot0[q] = atomicAdd(&ctl->sq_count[q], nq);
+      if (rs.sq_slot0[q] + nq > P->sq_cap[q]) {
+        atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
+        rs.sq_slot0[q] = kDone;
       }
     }
   }
@@ -557,6 +565,10 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     for (uint32_t i = lane; i < q.nchunks; i += 32) cm[i] = rslot;
   }
   sched_sync();  // the round's shared requests are consumed
+#ifdef TSQ_EXP_PHASE_CLOCK
+  TSQ_TCLK(w2);
+  if ((threadIdx.x & 31) == 0) atomicMax(&P->ctl->dbg[4], ((w1 - w0) << 32) | (w2 - w1));
+#endif
 }
 
 // CTA-wide appends (CTA mode: few segments, no contention to aggregate)
@@ -623,12 +635,6 @@ __device__ void cta_append_run(const Params *P, uint32_t kind, long long begin, 
   }
   sched_sync();
 }
-
-#ifdef TSQ_EXP_PHASE_CLOCK
-#define TSQ_TCLK(v) u64 v; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
-#else
-#define TSQ_TCLK(v) ((void)0)
-#endif
 
 // CTA mode: one CTA per (segment, child); the child-0 CTA also does the
 // segment's bookkeeping.
@@ -730,6 +736,7 @@ __device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
   }
   if (threadIdx.x < ST_COUNT) st[threadIdx.x] = 0ull;
   sched_sync();
+  TSQ_TCLK(q0);
   const long long avg = nseg ? ((long long)ctl->cur_ntiles * Geo<C, PAY>::TILE) / nseg : 0;
   if (avg >= kCtaScheduleMin) {
     for (uint32_t task = blockIdx.x; task < 2 * nseg; task += gridDim.x)
@@ -743,6 +750,7 @@ __device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
     }
   }
   sched_sync();
+  TSQ_TCLK(q1);
   if (threadIdx.x < ST_COUNT && st[threadIdx.x]) {
     u64 *dst[ST_COUNT] = {&ctl->stages, &ctl->sorted_bypass, &ctl->reversed_bypass,
                           &ctl->max_depth, &ctl->bytes_partition, &ctl->bytes_retire,
@@ -755,6 +763,10 @@ __device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
   if (threadIdx.x == 0) {
     __threadfence();
     const uint32_t d = atomicAdd(&ctl->ctas_done, 1u);
+#ifdef TSQ_EXP_PHASE_CLOCK
+    TSQ_TCLK(q2);
+    atomicMax(&ctl->dbg[7], ((q1 - q0) << 32) | (q2 - q1));
+#endif
     if (d == gridDim.x - 1) {
       __threadfence();
       const u64 packed = atomicExch(&ctl->next_packed, 0ull);
