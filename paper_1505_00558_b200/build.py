@@ -18,6 +18,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtsq_b200.so")
 TRACE_LIB = os.path.join(HERE, "libtsq_b200_trace.so")  # profiling build (-DTSQ_TRACE)
+# invariant-checked build (-DTSQ_DEBUG_CHECKS, scripts/gpu_debug_checks.sh)
+DEBUG_LIB = os.path.join(ROOT, "build_var", "libtsq_dbg.so")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -40,8 +42,10 @@ def up_to_date(lib: str = LIB) -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
-    lib = TRACE_LIB if trace else LIB
+def build(force: bool = False, verbose: bool = False, trace: bool = False,
+          debug_checks: bool = False) -> str:
+    lib = TRACE_LIB if trace else (DEBUG_LIB if debug_checks else LIB)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     if not force and up_to_date(lib):
         return lib
     cmd = [nvcc_path(), ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -49,6 +53,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
            os.path.join(CSRC, "tsq_capi.cu")]
     if trace:
         cmd.insert(1, "-DTSQ_TRACE")
+    if debug_checks:
+        cmd.insert(1, "-DTSQ_DEBUG_CHECKS")
     if verbose:
         cmd.insert(5, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
@@ -59,4 +65,4 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
-                trace="--trace" in sys.argv))
+                trace="--trace" in sys.argv, debug_checks="--debug-checks" in sys.argv))

@@ -32,6 +32,8 @@ __device__ __forceinline__ void emit_run(T *g, long long D, long long L, const T
   const long long b1 = (D + L) & ~(long long)(kAlign - 1);
   const long long base = D & ~(long long)(kAlign - 1);
   const bool body = b1 > b0;
+  TSQ_CHECK(!body || ((reinterpret_cast<uintptr_t>(g + b0) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(R + (b0 - base)) & 15) == 0));
   if (body && issuer)
     bulk_store(g + b0, R + (b0 - base), (uint32_t)((b1 - b0) * (long long)sizeof(T)));
   if ((int)(threadIdx.x >> 5) == scal_warp) {
@@ -398,6 +400,8 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   const long long ex_lt = (long long)(ex >> 31), ex_gt = (long long)(ex & 0x7fffffffull);
   const long long D_lt = begin + ex_lt;                    // first slot of this tile's < run
   const long long D_gt = m.end - ex_gt - (long long)t_gt;  // first slot of its > run
+  TSQ_CHECK(D_lt >= begin && D_lt + (long long)t_lt <= D_gt && D_gt >= begin &&
+            D_gt + (long long)t_gt <= m.end && m.end <= P->n);
   // records: the tile's first == payload slot in the side buffer
   const long long D_eq = P->reproducible ? lo - ex_lt - ex_gt : begin + (long long)m.eq_excl;
   const int o_lt = (int)(D_lt & (kAlign - 1));

@@ -151,6 +151,24 @@ struct StageRecord {
   int32_t depth;
 };
 
+// ---- invariant checks (debug builds only: -DTSQ_DEBUG_CHECKS) ---------------
+// compute-sanitizer is not available on the GPU pool; a debug build checks
+// the invariants every bulk copy, queue append and scatter relies on, and
+// traps (a sticky launch error the host reports) on the first violation.
+#ifdef TSQ_DEBUG_CHECKS
+#include <cstdio>
+#define TSQ_CHECK(cond)                                                                       \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("TSQ_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                              \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define TSQ_CHECK(cond) ((void)0)
+#endif
+
 // ---- optional per-tile timeline (profiling builds only: -DTSQ_TRACE) -------
 #ifdef TSQ_TRACE
 constexpr int kTraceTiles = 65536;

@@ -284,6 +284,8 @@ __global__ void __launch_bounds__(kThreads) retire_kernel(const Params *__restri
     __syncthreads();
     if (c >= total || c >= P->chunk_cap) break;
     const Run r = P->runs[P->chunkmap[c]];
+    TSQ_CHECK(r.begin >= 0 && r.begin + r.len <= P->n && c >= r.chunk_base &&
+              c < r.chunk_base + r.nchunks);
     const long long cc = (long long)(c - r.chunk_base);
     const long long lo = cc * kRunChunk;
     // every loop below issues kRB loads per thread before its stores, so

@@ -140,6 +140,7 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
     const long long tstart = (begin & ~(long long)(kAlign - 1)) + (long long)k * G::TILE;
     const long long lo = tstart > begin ? tstart : begin;
     const long long hi = (tstart + G::TILE) < end ? (tstart + G::TILE) : end;
+    TSQ_CHECK(lo < hi && hi <= P->n && lo - tstart >= 0 && hi - tstart <= G::TILE);
     const U *src = reinterpret_cast<const U *>(P->keys[buf]);
     const uint32_t *psrc = PAY ? P->pay[buf] : nullptr;
     U *dk = in_k + (size_t)s * G::SLOT;
@@ -174,6 +175,9 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
       m.has_next = hi < end ? 1u : 0u;  // verification: the counters read key hi
       TSQ_MARK(level, t, 1);
       if (tx) {
+        TSQ_CHECK((reinterpret_cast<uintptr_t>(src + a0) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(dk + (a0 - tstart)) & 15) == 0 &&
+                  a0 >= tstart - kAlign && a1 - tstart <= G::SLOT);
         mbar_arrive_expect_tx(&full[s], tx);
         bulk_load(dk + (a0 - tstart), src + a0, (uint32_t)((a1 - a0) * sizeof(U)), &full[s]);
         if (PAY) bulk_load(dp + (a0 - tstart), psrc + a0, (uint32_t)((a1 - a0) * 4), &full[s]);

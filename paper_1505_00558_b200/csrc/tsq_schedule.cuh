@@ -64,6 +64,7 @@ __device__ __forceinline__ void append_small(const Params *P, long long begin, l
                                              uint32_t buf) {
   Ctl *ctl = P->ctl;
   const int c = small_class(P, len);
+  TSQ_CHECK(len > 0 && len <= P->sq_lim[c] && begin >= 0 && begin + len <= P->n);
   const uint32_t slot = atomicAdd(&ctl->sq_count[c], 1u);
   if (slot < P->sq_cap[c]) {
     SmallSeg s;
@@ -436,6 +437,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
       }
     }
     const long long cb = c == 0 ? sg.begin : sg.end - gt;
+    TSQ_CHECK(lt >= 0 && gt >= 0 && lt + gt <= sg.end - sg.begin);
     const long long cl = c == 0 ? lt : gt;
     if (kids && cl > 0) {
       const uint32_t db = sg.buf ^ 1u;
@@ -675,6 +677,7 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
   {
     const int c = only;
     const long long cb = c == 0 ? sg.begin : sg.end - gt;
+    TSQ_CHECK(lt >= 0 && gt >= 0 && lt + gt <= sg.end - sg.begin);
     const long long cl = c == 0 ? lt : gt;
     if (cl <= 0) return;
     if (cl <= P->small_t) {

@@ -245,6 +245,7 @@ __device__ __forceinline__ void radix_run(const Params *P, const SmallSeg &sm,
         uint16_t *a = reinterpret_cast<uint16_t *>(mycb + ((uint32_t)(it[k] >> sh) & mask) * (2 * NT));
         const uint32_t r = *a;
         *a = (uint16_t)(r + 1u);
+        TSQ_CHECK(r < (uint32_t)(NA * KPT));
         buf[rpad((int)r)] = it[k];
         if (IDX) ibuf[rpad((int)r)] = ix[k];
       }
@@ -296,6 +297,7 @@ __device__ __forceinline__ void radix_sort_seg(const Params *P, const SmallSeg &
   const int len = sm.len;
   const U *src = reinterpret_cast<const U *>(P->keys[sm.buf]) + sm.begin;
   const bool raw = P->raw[sm.buf] != 0;
+  TSQ_CHECK(len >= 1 && len <= G::CAP && sm.begin >= 0 && sm.begin + len <= P->n);
   // coalesced load of the encoded keys into shared memory (slot rpad(i)),
   // taking the min / max on the way (explicit global loads, a batch in
   // flight before the first shared store: a generic load could alias the

@@ -4,6 +4,10 @@ against numpy (keys bit-exact under the device's total order; records:
 payload a permutation consistent with the keys).
 
     python scripts/fuzz.py [cases] [seed]
+    TSQ_FUZZ_TINY=1    cuts of 1-3 keys (the partition machine on tiny segments)
+    TSQ_FUZZ_BIG=1     2^22 .. 2^25 keys
+    TSQ_FUZZ_OFFSET=1  keys / payloads are CUDA views with a storage offset
+    TSQ_LIB=...        e.g. the -DTSQ_DEBUG_CHECKS build (scripts/gpu_debug_checks.sh)
 """
 import os
 import sys
@@ -72,7 +76,7 @@ for c in range(cases):
     if os.environ.get("TSQ_FUZZ_BIG") == "1":  # large inputs: 2^22 .. 2^25 keys
         n = int(rng.integers(1 << 22, 1 << 25))
     x, kind = keys_of(dt, n)
-    thr = int(rng.choice([0, 0, 0, 1, 3, 16, 4096, 8192, 16384]))
+    thr = int(rng.choice([0, 0, 0, 1, 3, 16, 4096, 8192, 16384, 24576, 32768]))
     if os.environ.get("TSQ_FUZZ_TINY") == "1":  # stress: the partition machine down to tiny segments
         thr = int(rng.choice([1, 2, 3]))
     rep = bool(rng.integers(0, 2))
@@ -82,12 +86,14 @@ for c in range(cases):
                                  fast_paths=os.environ.get("TSQ_FUZZ_NOFP") != "1"))
     if only >= 0 and c != only:
         continue
-    d = torch.from_numpy(x.copy()).cuda()
-    print(f"case {c}: dtype={np.dtype(dt).name} n={n} kind={kind} thr={thr} rep={rep} pay={pay}",
-          flush=True)
+    off = int(rng.integers(1, 4)) if os.environ.get("TSQ_FUZZ_OFFSET") == "1" else 0
+    # offset mode: the keys (and payload) are CUDA views with a storage offset
+    d = torch.from_numpy(np.concatenate([x[:off], x]).copy()).cuda()[off:]
+    print(f"case {c}: dtype={np.dtype(dt).name} n={n} kind={kind} thr={thr} rep={rep} pay={pay} "
+          f"off={off}", flush=True)
     try:
         if pay:
-            p = torch.arange(n, dtype=torch.int64).to(torch.uint32).cuda()
+            p = torch.arange(-off, n, dtype=torch.int64).to(torch.uint32).cuda()[off:]
             s.sort(T.Records(d, p))
             ko, po = d.cpu().numpy(), p.cpu().numpy().astype(np.int64)
             ok = ko.tobytes() == total_order_sorted(x).tobytes() and \
