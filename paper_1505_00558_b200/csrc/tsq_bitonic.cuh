@@ -85,13 +85,13 @@ __device__ __forceinline__ void exchange(const SortItem<U, PAY> (&v)[E], SortIte
       if (PAY) y[r].i = __shfl_xor_sync(0xffffffffu, s.i, m);
     }
   } else {
-    sched_sync();
+    __syncthreads();
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       xk[r * kThreads + tid] = v[r].k;
       if (PAY) xi[r * kThreads + tid] = v[r].i;
     }
-    sched_sync();
+    __syncthreads();
     const int p = tid ^ m;
 #pragma unroll
     for (int r = 0; r < E; ++r) {

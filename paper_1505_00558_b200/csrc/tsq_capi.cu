@@ -20,9 +20,9 @@ using namespace tsq;
 namespace {
 
 struct KernelSet {
-  const void *init, *part, *retire, *selp, *exportk;
+  const void *init, *part, *sched, *retire, *selp, *exportk;
   int key_bytes, tile;
-  size_t part_smem;
+  size_t part_smem, sched_smem;
   // on-chip sort classes: 256 / 512 threads (tsq_small.cuh)
   const void *small[kSmallClasses];
   size_t small_smem[kSmallClasses];
@@ -54,6 +54,7 @@ KernelSet make_set() {
   KernelSet s;
   s.init = reinterpret_cast<const void *>(&init_kernel<C, PAY>);
   s.part = reinterpret_cast<const void *>(&partition_kernel<C, PAY>);
+  s.sched = reinterpret_cast<const void *>(&schedule_kernel<C, PAY>);
   s.small[0] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, kThreads>);
   s.small[1] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 2 * kThreads>);
   s.small_smem[0] = RadixGeo<C, PAY, kThreads>::SMEM;
@@ -71,6 +72,7 @@ KernelSet make_set() {
   s.key_bytes = (int)sizeof(U);
   s.tile = Geo<C, PAY>::TILE;
   s.part_smem = Geo<C, PAY>::SMEM;
+  s.sched_smem = (size_t)(kThreads / 32) * (kMaxSample + 1) * sizeof(U);
   return s;
 }
 
@@ -251,34 +253,39 @@ int occupancy_grid(tsq_workspace *ws, const void *fn, size_t smem, int block = k
 }
 
 tsq_status prepare_small_smem(const KernelSet &ks) {
-  const void *fns[1 + kSmallClasses] = {ks.part, ks.small[0], ks.small[1], ks.small[2]};
-  const size_t sm[1 + kSmallClasses] = {ks.part_smem, ks.small_smem[0], ks.small_smem[1],
-                                        ks.small_smem[2]};
+  const void *fns[2 + kSmallClasses] = {ks.part, ks.sched, ks.small[0], ks.small[1], ks.small[2]};
+  const size_t sm[2 + kSmallClasses] = {ks.part_smem, ks.sched_smem, ks.small_smem[0],
+                                        ks.small_smem[1], ks.small_smem[2]};
   // always opt in: dynamic + static shared memory may cross 48 KB even when
   // the dynamic part alone does not
-  for (int i = 0; i < 1 + kSmallClasses; ++i)
+  for (int i = 0; i < 2 + kSmallClasses; ++i)
     if (fns[i]) TSQ_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sm[i]));
   return TSQ_OK;
 }
 
-// one recursion level = one level kernel (partition pass, grid barrier,
-// segment scheduling), launched cooperatively so every CTA is resident
+// one recursion level = partition pass + segment scheduling
 struct LevelLaunch {
-  dim3 part_grid;
+  dim3 part_grid, sched_grid;
 };
 
 LevelLaunch level_launch(tsq_workspace *ws, const KernelSet &ks) {
   LevelLaunch L;
   L.part_grid = dim3(occupancy_grid(ws, ks.part, ks.part_smem, kPartThreads));
+#ifdef TSQ_SCHED_PER_SM
+  L.sched_grid = dim3(TSQ_SCHED_PER_SM * ws->num_sms);
+#else
+  L.sched_grid = dim3(occupancy_grid(ws, ks.sched, ks.sched_smem));
+#endif
   return L;
 }
 
 cudaError_t launch_level(const KernelSet &ks, const LevelLaunch &L, Params **dst,
                          cudaStream_t s) {
   void *args[1] = {dst};
-  return cudaLaunchCooperativeKernel(ks.part, L.part_grid, dim3(kPartThreads), args, ks.part_smem,
-                                     s);
+  cudaError_t e = cudaLaunchKernel(ks.part, L.part_grid, dim3(kPartThreads), args, ks.part_smem, s);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernel(ks.sched, L.sched_grid, dim3(kThreads), args, ks.sched_smem, s);
 }
 
 // the on-chip sort classes, retirement and the queue reset (a drain round)
@@ -341,9 +348,9 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
 }
 
 // The whole sort as one graph, no host round trip per level:
-//   init -> WHILE(outer) { WHILE(inner) { level kernel }
+//   init -> WHILE(outer) { WHILE(inner) { partition -> schedule }
 //                          -> small sorts || retire -> drain }
-// The last CTA of a level kernel keeps the inner loop going while
+// The last schedule CTA of a level keeps the inner loop going while
 // segments remain; when the on-chip or run queues could not take another
 // level it ends the inner loop early (a flush), the drain round empties
 // them and the outer loop re-enters the level loop.  Normally the outer
@@ -356,7 +363,7 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   for (int i = 0; i < 3; ++i) TSQ_CUDA(cudaEventCreate(&ge->ev[i]));
   TSQ_CUDA(cudaGraphCreate(&ge->graph, 0));
   cudaGraph_t g = ge->graph;
-  cudaGraphNode_t e0, e1, e2, onode, inode, lnode;
+  cudaGraphNode_t e0, e1, e2, onode, inode, lnode, schednode;
   TSQ_CUDA(cudaGraphAddEventRecordNode(&e0, g, nullptr, 0, ge->ev[0]));
 
   static Params dummy;  // replaced per call via cudaGraphExecKernelNodeSetParams
@@ -408,16 +415,13 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   pk.sharedMemBytes = (unsigned)ks.part_smem;
   pk.kernelParams = dev_args;
   TSQ_CUDA(cudaGraphAddKernelNode(&lnode, body, nullptr, 0, &pk));
-  {
-    // the level kernel's grid barrier needs every CTA resident
-    cudaKernelNodeAttrValue coop;
-    memset(&coop, 0, sizeof(coop));
-    coop.cooperative = 1;
-    TSQ_CUDA(cudaGraphKernelNodeSetAttribute(lnode, cudaLaunchAttributeCooperative, &coop));
-  }
   cudaKernelNodeParams lk = cudaKernelNodeParams{};
+  lk.func = const_cast<void *>(ks.sched);
+  lk.gridDim = LL.sched_grid;
   lk.blockDim = dim3(kThreads);
+  lk.sharedMemBytes = (unsigned)ks.sched_smem;
   lk.kernelParams = dev_args;
+  TSQ_CUDA(cudaGraphAddKernelNode(&schednode, body, &lnode, 1, &lk));
 
   cudaGraphNode_t tail[kSmallClasses + 1];
   int ntail = 0;
@@ -819,23 +823,9 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
       if (st != TSQ_OK) return st;
     }
     if (getenv("TSQ_DEBUG_LEVELS"))
-      fprintf(stderr, "tsq level %d: segments %u tiles %u small %u/%u runs %u error %u "
-              "phase us: part-spread %.1f barrier %.1f sched %.1f\n", lv,
+      fprintf(stderr, "tsq level %d: segments %u tiles %u small %u/%u runs %u error %u\n", lv,
               ws->h_ctl->cur_nseg, ws->h_ctl->cur_ntiles, ws->h_ctl->sq_count[0],
-              ws->h_ctl->sq_count[1], (uint32_t)(ws->h_ctl->run_packed >> 32), ws->h_ctl->error,
-              (ws->h_ctl->dbg[1] - ws->h_ctl->dbg[0]) * 1e-3, (ws->h_ctl->dbg[2] - ws->h_ctl->dbg[1]) * 1e-3,
-              (ws->h_ctl->dbg[3] - ws->h_ctl->dbg[2]) * 1e-3);
-    if (getenv("TSQ_DEBUG_LEVELS"))
-      fprintf(stderr, "   cta task / sched ns: head|tasks %llu pivot|end %llu append %llu\n",
-              ws->h_ctl->dbg[5] >> 40, (ws->h_ctl->dbg[5] >> 20) & 0xfffff, ws->h_ctl->dbg[5] & 0xfffff);
-    if (getenv("TSQ_DEBUG_LEVELS"))
-      fprintf(stderr, "   warp round ns: tasks %llu claims+writes %llu | sched loop %llu end %llu\n",
-              ws->h_ctl->dbg[4] >> 32, ws->h_ctl->dbg[4] & 0xffffffffull,
-              ws->h_ctl->dbg[7] >> 32, ws->h_ctl->dbg[7] & 0xffffffffull);
-    if (getenv("TSQ_DEBUG_LEVELS")) {  // reset the phase timers for the next level
-      TSQ_CUDA(cudaMemsetAsync(&ws->d_ctl->dbg[0], 0, 8 * sizeof(u64), s));
-      TSQ_CUDA(cudaMemsetAsync(&ws->d_ctl->dbg[0], 0xff, sizeof(u64), s));
-    }
+              ws->h_ctl->sq_count[1], (uint32_t)(ws->h_ctl->run_packed >> 32), ws->h_ctl->error);
     if (ws->h_ctl->cur_nseg == 0 || ws->h_ctl->error) break;
     const uint32_t nseg = ws->h_ctl->cur_nseg;
     ws->level_segs.push_back(nseg);
@@ -844,13 +834,13 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
     snprintf(name, sizeof(name), "tsq level %d", lv);
     NvtxRange lvl(name);
     TSQ_CUDA(cudaEventRecord(e0, s));
-    TSQ_CUDA(cudaLaunchCooperativeKernel(ks.part, LL.part_grid, dim3(kPartThreads), largs,
-                                         ks.part_smem, s));
+    TSQ_CUDA(cudaLaunchKernel(ks.part, LL.part_grid, dim3(kPartThreads), largs, ks.part_smem, s));
     TSQ_CUDA(cudaEventRecord(em, s));
     if (exporting) {
       const unsigned g = nseg < 4u * (unsigned)ws->num_sms ? nseg : 4u * (unsigned)ws->num_sms;
       TSQ_CUDA(cudaLaunchKernel(ks.exportk, dim3(g), dim3(kThreads), largs, 0, s));
     }
+    TSQ_CUDA(cudaLaunchKernel(ks.sched, LL.sched_grid, dim3(kThreads), largs, ks.sched_smem, s));
     TSQ_CUDA(cudaEventRecord(e1, s));
     TSQ_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f, ms2 = 0.f;

@@ -484,9 +484,6 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   }
 }
 
-// The level kernel: one recursion level -- the partition pass (the
-// warp-specialised pipeline above), a grid barrier, then the segment
-// scheduling of tsq_schedule.cuh -- in one cooperative launch.
 template <class C, bool PAY>
 __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ Pg) {
   typedef typename C::U U;
@@ -524,54 +521,28 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
   const int warp = threadIdx.x >> 5;
   if (warp == kProducerWarp) {
     producer_loop<C, PAY>(P, cur, ntiles, in_k, in_p, full, aggr, empty, meta);
-  } else if (warp >= kCounterWarp) {
+    return;
+  }
+  if (warp >= kCounterWarp) {
     counter_loop<C, PAY>(P, cur, in_k, full, aggr, empty, meta, sc, cshare,
                          warp - kCounterWarp);
-  } else if (warp >= kLookbackWarp) {
+    return;
+  }
+  if (warp >= kLookbackWarp) {
     lookback_loop<PAY, G::STAGES>(P, cur, aggr, ready, meta, warp - kLookbackWarp);
-  } else {
-    int pend = -1;  // (thread 0) the stage the last bulk stores may still be reading
-    for (uint32_t k = 0;; ++k) {
-      const int s = (int)(k % G::STAGES);
-      wait_ready_consumer(&ready[s], (k / G::STAGES) & 1u);
-      if (meta[s].kind == KIND_DONE) break;
-      emit_tile<C, PAY>(P, k, in_k, in_p, empty, meta, sc, pend);
-    }
-    if (threadIdx.x == 0) {
-      bulk_wait0();
-      if (pend >= 0) mbar_arrive(&empty[pend]);
-    }
+    return;
   }
-  // Grid barrier (the launch is cooperative: every CTA is resident): the
-  // level's partition output is complete everywhere before any segment is
-  // scheduled.  Then warps 0-7 schedule the level's segments in the ring's
-  // shared memory.
-  __syncthreads();
-#ifdef TSQ_EXP_PHASE_CLOCK
-  u64 tp0, tp1, tp2;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0));
-#endif
+  int pend = -1;  // (thread 0) the stage the last bulk stores may still be reading
+  for (uint32_t k = 0;; ++k) {
+    const int s = (int)(k % G::STAGES);
+    wait_ready_consumer(&ready[s], (k / G::STAGES) & 1u);
+    if (meta[s].kind == KIND_DONE) break;
+    emit_tile<C, PAY>(P, k, in_k, in_p, empty, meta, sc, pend);
+  }
   if (threadIdx.x == 0) {
-    fence_proxy_async_global();  // this CTA's bulk-store writes
-    __threadfence();
-    atomicAdd(&ctl->gbar, 1u);
-    while (ld_volatile32(&ctl->gbar) < gridDim.x) __nanosleep(64);
-    __threadfence();
+    bulk_wait0();
+    if (pend >= 0) mbar_arrive(&empty[pend]);
   }
-  __syncthreads();
-#ifdef TSQ_EXP_PHASE_CLOCK
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
-#endif
-  if (warp < kThreads / 32) schedule_phase<C, PAY>(P, level, smem_raw);
-#ifdef TSQ_EXP_PHASE_CLOCK
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp2));
-  if (threadIdx.x == 0) {
-    atomicMin(&ctl->dbg[0], tp0);   // first CTA done partitioning
-    atomicMax(&ctl->dbg[1], tp0);   // last CTA done partitioning
-    atomicMax(&ctl->dbg[2], tp1);   // barrier released
-    atomicMax(&ctl->dbg[3], tp2);   // last schedule phase done
-  }
-#endif
 }
 
 }  // namespace tsq

@@ -101,9 +101,6 @@ struct Ctl {
   uint32_t flush, flushes;
   u64 small_segs_done;      // on-chip segments of earlier flush rounds
   u64 bisected;             // segments split at their key-bound midpoint
-  uint32_t gbar;            // level kernel: CTAs through the partition phase
-  uint32_t prev_nseg;       // segments of the level before `level` (stage export)
-  u64 dbg[8];               // experiment timers (TSQ_EXP_PHASE_CLOCK)
 };
 
 // Everything a kernel needs; lives in device memory, written by the init
@@ -381,34 +378,12 @@ __device__ __forceinline__ void bulk_wait_read1() {
 __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
-// async-proxy (bulk copy) writes to global memory -> ordered before this
-// thread's later generic-proxy operations (SASS FENCE.VIEW.ASYNC.G)
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 // generic-proxy smem writes -> visible to the async (bulk copy) proxy
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-// The segment-scheduling code runs on the first kThreads threads of a CTA
-// (the whole CTA of the init kernel; warps 0-7 of a level kernel after its
-// partition phase): its CTA-wide syncs are named barrier kSchedBar.
-constexpr uint32_t kSchedBar = 3;
-__device__ __forceinline__ void sched_sync() { named_sync(kSchedBar, kThreads); }
-__device__ __forceinline__ bool sched_sync_and(bool v) {
-  uint32_t r;
-  asm volatile(
-      "{\n\t.reg .pred q, p;\n\t"
-      "setp.ne.u32 q, %1, 0;\n\t"
-      "barrier.cta.red.and.pred p, %2, %3, q;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(r)
-      : "r"(v ? 1u : 0u), "r"(kSchedBar), "r"((uint32_t)kThreads)
-      : "memory");
-  return r != 0;
 }
 
 __device__ __forceinline__ u64 warp_sum64(u64 v) {

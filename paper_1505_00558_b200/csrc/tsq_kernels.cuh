@@ -15,13 +15,11 @@
 //                      < run from the segment front and the > run from the
 //                      back.  Segments whose samples looked sorted/reversed
 //                      are verified instead (core.py:1678-1698 fast paths).
-//                      After a grid barrier (cooperative launch) the same
-//                      kernel schedules the level (tsq_schedule.cuh): one
-//                      warp (or CTA) per child of each segment retires the
-//                      ==p run, samples the children's pivots
-//                      (pivot.py:205-248) and queues them for the next level
-//                      or the on-chip sort (core.py:1711-1728); the last CTA
-//                      advances the level and sets the CUDA-graph loop
+//   schedule_kernel    one warp (or CTA) per child of each segment of the
+//                      level: retires the ==p run, samples the children's
+//                      pivots (pivot.py:205-248) and queues them for the next
+//                      level or the on-chip sort (core.py:1711-1728); the last
+//                      CTA advances the level and sets the CUDA-graph loop
 //                      condition
 //   small_sort_kernel  on-chip sort of segments <= small_t (insertion_sort's
 //                      role, smallsort.py:12-47): LSD radix sort over the
@@ -111,9 +109,9 @@ struct StageMeta {
 
 }  // namespace tsq
 
+#include "tsq_partition.cuh"
 #include "tsq_small.cuh"
 #include "tsq_schedule.cuh"
-#include "tsq_partition.cuh"
 #include "tsq_gather.cuh"
 
 namespace tsq {
@@ -192,10 +190,9 @@ __global__ void drain_kernel(const Params *__restrict__ P) {
   }
 }
 
-// Stage export (stage_hook / trace mode, host-driven levels): after a level
-// kernel (which has already advanced the level), write every segment of the
-// level it partitioned -- its post-stage contents into the caller's buffers
-// (the view) and its record --
+// Stage export (stage_hook / trace mode, host-driven levels): between a
+// level's partition pass and its scheduling, write every segment's
+// post-stage contents into the caller's buffers (the view) and its record --
 // the state the reference's hook sees after each stage (core.py:1705-1710).
 // One CTA per segment; debug path, plain loads and stores.
 template <class C, bool PAY>
@@ -203,8 +200,8 @@ __global__ void __launch_bounds__(kThreads) export_level_kernel(const Params *__
   typedef typename C::U U;
   __shared__ u64 s_cnt[2];
   const Ctl *ctl = P->ctl;
-  const int cur = (int)((ctl->level - 1u) & 1u);  // the level just partitioned
-  const uint32_t nseg = ctl->prev_nseg;
+  const int cur = (int)(ctl->level & 1u);
+  const uint32_t nseg = ctl->cur_nseg;
   U *vk = reinterpret_cast<U *>(P->view_keys);
   uint32_t *vp = P->view_pay;
   for (uint32_t sid = blockIdx.x; sid < nseg; sid += gridDim.x) {

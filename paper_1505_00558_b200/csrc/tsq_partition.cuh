@@ -81,12 +81,10 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
   uint32_t *ticket = &P->ctl->tile_ticket;
   const uint32_t grid = gridDim.x;
   TileSeg mine;  // lane j: the tile c0 + j of the current chunk
-  // current chunk [c0, c0 + cn) at position ci; the next one, claimed ahead
-  uint32_t c0 = 0, cn = 0, ci = 0, n0 = 0, nn = 0;
-  if (lane == 0) {
-    nn = guided_chunk(0u, ntiles, grid);
-    n0 = atomicAdd(ticket, nn);
-  }
+  // current chunk [c0, c0 + cn) at position ci; the next one, claimed ahead.
+  // Tile b of the level is CTA b's without a claim (the ticket counts from
+  // tile G), so a level of <= G tiles takes no atomic at all.
+  uint32_t c0 = 0, cn = 0, ci = 0, n0 = blockIdx.x, nn = 1;
   for (uint32_t it = 0;; ++it) {
     const int s = (int)(it % G::STAGES);
     const uint32_t j = it / G::STAGES;
@@ -95,9 +93,11 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
       c0 = __shfl_sync(0xffffffffu, n0, 0);
       cn = __shfl_sync(0xffffffffu, nn, 0);
       ci = 0;
-      if (lane == 0 && c0 < ntiles) {
-        nn = guided_chunk(c0 + cn, ntiles, grid);
-        n0 = atomicAdd(ticket, nn);
+      if (lane == 0 && c0 < ntiles && grid < ntiles) {
+        nn = guided_chunk(c0 + cn > grid ? c0 + cn : grid, ntiles, grid);
+        n0 = grid + atomicAdd(ticket, nn);
+      } else if (lane == 0) {
+        n0 = ntiles;  // nothing left to claim
       }
       const uint32_t tl = c0 + (uint32_t)lane;
       mine = resolve_tile(P, cur, (lane < (int)cn && tl < ntiles) ? tl : ntiles, ntiles);

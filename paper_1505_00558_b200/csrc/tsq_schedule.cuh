@@ -17,12 +17,6 @@
 
 namespace tsq {
 
-// experiment timers (TSQ_EXP_PHASE_CLOCK builds only)
-#ifdef TSQ_EXP_PHASE_CLOCK
-#define TSQ_TCLK(v) u64 v; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
-#else
-#define TSQ_TCLK(v) ((void)0)
-#endif
 
 
 // per-CTA statistics (shared-memory atomics, one global flush per CTA)
@@ -250,28 +244,28 @@ __device__ typename C::U cta_select_pivot_fast(const typename C::U *data, bool e
       desc &= raw[q] >= raw[q + 1];
     }
   xk[tid] = raw[0];
-  sched_sync();
+  __syncthreads();
   if (tid < kThreads - 1 && (tid + 1) * Q < S) {
     asc &= raw[Q - 1] <= xk[tid + 1];
     desc &= raw[Q - 1] >= xk[tid + 1];
   }
-  asc = sched_sync_and(asc);
-  desc = sched_sync_and(desc);
+  asc = __syncthreads_and(asc);
+  desc = __syncthreads_and(desc);
   *flag = asc ? 1 : (desc ? -1 : 0);
   SortItem<U, false> v[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) v[q].k = raw[q];
   block_bitonic<U, false, Q>(v, xk, nullptr);
   const int midi = S >> 1;
-  sched_sync();
+  __syncthreads();
   if (tid == midi / Q) {
 #pragma unroll
     for (int q = 0; q < Q; ++q)
       if (q == midi % Q) xk[0] = v[q].k;
   }
-  sched_sync();
+  __syncthreads();
   const U piv = xk[0];
-  sched_sync();
+  __syncthreads();
   (void)bc;
   return piv;
 }
@@ -401,7 +395,6 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     rs.run[warp].valid = 0;
   }
   __syncwarp();
-  TSQ_TCLK(w0);
   if (have) {
     const uint32_t sid = task >> 1;
     const int c = (int)(task & 1u);
@@ -472,8 +465,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
       }
     }
   }
-  TSQ_TCLK(w1);
-  sched_sync();
+  __syncthreads();
   // one claim per queue for the whole round, the queues' atomics issued by
   // separate lanes of warp 0 so their round trips overlap
   if (threadIdx.x < 2 + kSmallClasses) {
@@ -511,7 +503,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
       }
     }
   }
-  sched_sync();
+  __syncthreads();
   // each warp writes its records at its offsets
   uint32_t lslot = rs.lv_slot0, ltile = rs.lv_tile0, rslot = rs.run_slot0;
   uint32_t rchunk = rs.run_chunk0;
@@ -566,11 +558,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     uint32_t *cm = P->chunkmap + rchunk;
     for (uint32_t i = lane; i < q.nchunks; i += 32) cm[i] = rslot;
   }
-  sched_sync();  // the round's shared requests are consumed
-#ifdef TSQ_EXP_PHASE_CLOCK
-  TSQ_TCLK(w2);
-  if ((threadIdx.x & 31) == 0) atomicMax(&P->ctl->dbg[4], ((w1 - w0) << 32) | (w2 - w1));
-#endif
+  __syncthreads();  // the round's shared requests are consumed
 }
 
 // CTA-wide appends (CTA mode: few segments, no contention to aggregate)
@@ -599,13 +587,13 @@ __device__ void cta_append_level(const Params *P, int nxt, long long begin, long
     bc[0] = slot;
     bc[1] = tbase;
   }
-  sched_sync();
+  __syncthreads();
   const uint32_t slot = bc[0], tbase = bc[1];
   if (slot != kDone) {
     uint32_t *tm = P->tilemap[nxt] + tbase;
     for (uint32_t i = threadIdx.x; i < ntiles; i += kThreads) tm[i] = slot;
   }
-  sched_sync();
+  __syncthreads();
 }
 
 __device__ void cta_append_run(const Params *P, uint32_t kind, long long begin, long long len,
@@ -629,13 +617,13 @@ __device__ void cta_append_run(const Params *P, uint32_t kind, long long begin, 
     bc[0] = slot;
     bc[1] = cbase;
   }
-  sched_sync();
+  __syncthreads();
   const uint32_t slot = bc[0], cbase = bc[1];
   if (slot != kDone) {
     uint32_t *cm = P->chunkmap + cbase;
     for (uint32_t i = threadIdx.x; i < nchunks; i += kThreads) cm[i] = slot;
   }
-  sched_sync();
+  __syncthreads();
 }
 
 // CTA mode: one CTA per (segment, child); the child-0 CTA also does the
@@ -646,14 +634,12 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
   typedef typename C::U U;
   const uint32_t sid = task >> 1;
   const int only = (int)(task & 1u);
-  TSQ_TCLK(c0);
   const Seg sg = P->segs[cur][sid];
   long long lt = 0, gt = 0;
   uint32_t requeue = 0;
   const bool kids =
       segment_head<C, PAY, true>(P, nxt, sg, cur, st, &lt, &gt, &requeue, only == 0);
-  sched_sync();
-  TSQ_TCLK(c1);
+  __syncthreads();
   const long long len = sg.end - sg.begin;
   if (only == 1) {
     if (!kids) return;
@@ -695,40 +681,25 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
       piv = bisect_pivot(klo, khi);
       if (threadIdx.x == 0) atomicAdd(&st[ST_BISECTED], 1ull);
     } else {
-      TSQ_TCLK(c2a);
       piv = (u64)cta_select_pivot_fast<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
                                           cb, cl, P->dran, P->mitigation, xk, bc, &flag);
     }
     uint32_t kind = KIND_PARTITION;
     if (P->fast_paths)
       kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
-    TSQ_TCLK(c2);
     cta_append_level<C, PAY>(P, nxt, cb, cb + cl, db, piv, klo, khi, kind, depth, 0, bc);
-#ifdef TSQ_EXP_PHASE_CLOCK
-    TSQ_TCLK(c3);
-    if (threadIdx.x == 0) {
-      atomicMax(&P->ctl->dbg[5], ((c1 - c0) << 40) | ((c2 - c1) << 20) | (c3 - c2));
-    }
-#endif
   }
 }
 
-// The scheduling phase of a level kernel (tsq_consume.cuh), after the grid
-// barrier that ends its partition phase: warps 0-7 of every CTA take the
-// level's (segment, child) tasks -- a CTA per child while the average
-// segment has >= 2^20 keys, a warp per child below -- then the last CTA
-// publishes the next level and sets the graph's loop condition.  `smem`: the
-// partition ring, free now (sample buffer, round requests, statistics).
 template <class C, bool PAY>
-__device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
-                                               unsigned char *smem) {
+__global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__restrict__ P) {
   typedef typename C::U U;
-  constexpr size_t kXk = (size_t)(kThreads / 32) * (kMaxSample + 1) * sizeof(U);
-  U *xk = reinterpret_cast<U *>(smem);
-  RoundShared &rs = *reinterpret_cast<RoundShared *>(smem + kXk);
-  u64 *st = reinterpret_cast<u64 *>(smem + kXk + ((sizeof(RoundShared) + 15) & ~(size_t)15));
-  volatile uint32_t *bcast = reinterpret_cast<volatile uint32_t *>(st + ST_COUNT);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ u64 st[ST_COUNT];
+  __shared__ uint32_t bcast[2];
+  __shared__ RoundShared rs;
   Ctl *ctl = P->ctl;
+  const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u), nxt = cur ^ 1;
   const uint32_t nseg = ctl->cur_nseg;
   {
@@ -738,10 +709,10 @@ __device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
       lbn[i] = 0ull;
   }
   if (threadIdx.x < ST_COUNT) st[threadIdx.x] = 0ull;
-  sched_sync();
-  TSQ_TCLK(q0);
+  __syncthreads();
   const long long avg = nseg ? ((long long)ctl->cur_ntiles * Geo<C, PAY>::TILE) / nseg : 0;
   if (avg >= kCtaScheduleMin) {
+    U *xk = reinterpret_cast<U *>(smem_raw);
     for (uint32_t task = blockIdx.x; task < 2 * nseg; task += gridDim.x)
       schedule_segment_cta<C, PAY>(P, cur, nxt, task, xk, st, bcast);
   } else {
@@ -752,8 +723,7 @@ __device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
       schedule_round_warp<C, PAY>(P, cur, nxt, task, task < ntask, st, rs);
     }
   }
-  sched_sync();
-  TSQ_TCLK(q1);
+  __syncthreads();
   if (threadIdx.x < ST_COUNT && st[threadIdx.x]) {
     u64 *dst[ST_COUNT] = {&ctl->stages, &ctl->sorted_bypass, &ctl->reversed_bypass,
                           &ctl->max_depth, &ctl->bytes_partition, &ctl->bytes_retire,
@@ -766,20 +736,14 @@ __device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
   if (threadIdx.x == 0) {
     __threadfence();
     const uint32_t d = atomicAdd(&ctl->ctas_done, 1u);
-#ifdef TSQ_EXP_PHASE_CLOCK
-    TSQ_TCLK(q2);
-    atomicMax(&ctl->dbg[7], ((q1 - q0) << 32) | (q2 - q1));
-#endif
     if (d == gridDim.x - 1) {
       __threadfence();
       const u64 packed = atomicExch(&ctl->next_packed, 0ull);
       const uint32_t ns = (uint32_t)(packed >> 32), nt = (uint32_t)packed;
-      ctl->prev_nseg = nseg;
       ctl->cur_nseg = ns;
       ctl->cur_ntiles = nt;
       ctl->tile_ticket = 0;
       ctl->ctas_done = 0;
-      ctl->gbar = 0;  // every CTA is past this level's grid barrier
       ctl->level = level + 1;
       ctl->levels += 1;
       bool more = ns > 0;
@@ -790,9 +754,8 @@ __device__ __forceinline__ void schedule_phase(const Params *P, uint32_t level,
       if (ctl->error) more = false;
       // drain the on-chip and run queues before a level could overflow them:
       // one level appends at most 2 * seg_cap small segments and seg_cap runs
-      // (the larger on-chip classes cannot overflow: their segments are
-      // disjoint and longer than the small class's capacity, sq_cap[1..] > n
-      // / that)
+      // (the large on-chip class cannot overflow: its segments are disjoint
+      // and longer than the small class's capacity, sq_cap[1] > n / that)
       const uint32_t runs = (uint32_t)(ctl->run_packed >> 32);
       const bool flush = more && (ctl->sq_count[0] + 2u * P->seg_cap > P->sq_cap[0] ||
                                   runs + P->seg_cap > P->run_cap);
