@@ -43,8 +43,10 @@ int key_bytes_of(int dt);
 // 8192, 4.98 at 16384; records 2^27: 9.79 / 9.90 ms).
 int default_small_t(int kt, int pt, size_t n) {
   const bool pay = pt == TSQ_U32;
-  if (key_bytes_of(kt) == 4 && !pay) return n <= (1u << 21) ? kSmallMax : kSmallGiant;
-  return kSmallMax;
+  // (a class of S item slots takes segments of <= S - kSmallSlack keys)
+  if (key_bytes_of(kt) == 4 && !pay)
+    return (n <= (1u << 21) ? kSmallMax : kSmallGiant) - kSmallSlack;
+  return kSmallMax - kSmallSlack;
 }
 
 template <int DT, bool PAY>
@@ -55,16 +57,18 @@ KernelSet make_set() {
   s.init = reinterpret_cast<const void *>(&init_kernel<C, PAY>);
   s.part = reinterpret_cast<const void *>(&partition_kernel<C, PAY>);
   s.sched = reinterpret_cast<const void *>(&schedule_kernel<C, PAY>);
-  s.small[0] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, kThreads>);
-  s.small[1] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 2 * kThreads>);
-  s.small_smem[0] = RadixGeo<C, PAY, kThreads>::SMEM;
-  s.small_smem[1] = RadixGeo<C, PAY, 2 * kThreads>::SMEM;
-  for (int c = 0; c < kSmallClasses; ++c) s.small_threads[c] = kThreads << c;
-  s.small_cap[0] = RadixGeo<C, PAY, kThreads>::CAP;
-  s.small_cap[1] = RadixGeo<C, PAY, 2 * kThreads>::CAP;
-  s.small[2] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 4 * kThreads>);
-  s.small_smem[2] = RadixGeo<C, PAY, 4 * kThreads>::SMEM;
-  s.small_cap[2] = RadixGeo<C, PAY, 4 * kThreads>::CAP;
+  s.small[0] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 0>);
+  s.small[1] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 1>);
+  s.small[2] = reinterpret_cast<const void *>(&small_sort_kernel<C, PAY, 2>);
+  s.small_smem[0] = RadixGeo<C, PAY, 0>::SMEM;
+  s.small_smem[1] = RadixGeo<C, PAY, 1>::SMEM;
+  s.small_smem[2] = RadixGeo<C, PAY, 2>::SMEM;
+  s.small_threads[0] = RadixGeo<C, PAY, 0>::NT;
+  s.small_threads[1] = RadixGeo<C, PAY, 1>::NT;
+  s.small_threads[2] = RadixGeo<C, PAY, 2>::NT;
+  s.small_cap[0] = RadixGeo<C, PAY, 0>::CAP;
+  s.small_cap[1] = RadixGeo<C, PAY, 1>::CAP;
+  s.small_cap[2] = RadixGeo<C, PAY, 2>::CAP;
   s.raw_order = C::kRawOrder;
   s.retire = reinterpret_cast<const void *>(&retire_kernel<C, PAY>);
   s.selp = reinterpret_cast<const void *>(&select_pivot_kernel<C>);
@@ -85,7 +89,7 @@ bool get_set(int dt, bool pay, KernelSet *out) {
   if (dt * 2 + (pay ? 1 : 0) != TSQ_ONLY) return false;
   *out = make_set<TSQ_ONLY / 2, (TSQ_ONLY & 1) != 0>();
   return true;
-#endif
+#else
   switch (dt) {
     TSQ_CASE(TSQ_I32)
     TSQ_CASE(TSQ_U32)
@@ -96,6 +100,7 @@ bool get_set(int dt, bool pay, KernelSet *out) {
     default:
       return false;
   }
+#endif
 #undef TSQ_CASE
 }
 
@@ -143,8 +148,8 @@ Layout make_layout(size_t n, int kt, int pt, int small_t = 0, bool staged = fals
   L.tile_cap = (uint32_t)(n / tile + 2ull * L.seg_cap + 2);
   L.run_cap = 8u * L.seg_cap + 64u;
   L.sq_cap[0] = 2u * L.run_cap;
-  L.sq_cap[1] = (uint32_t)(n / (size_t)(kSmallT + 1) + 2);
-  L.sq_cap[2] = (uint32_t)(n / (size_t)(kSmallMax + 1) + 2);
+  L.sq_cap[1] = (uint32_t)(n / (size_t)(kSmallT - kSmallSlack + 1) + 2);
+  L.sq_cap[2] = (uint32_t)(n / (size_t)(kSmallMax - kSmallSlack + 1) + 2);
   if (getenv("TSQ_DEBUG_MIN_QUEUES")) {
     // test knob: the smallest queues the flush rule allows, so the level
     // loop drains them every level or two (exercises the drain rounds)
@@ -340,10 +345,10 @@ void fill_params(tsq_workspace *ws, const Layout &L, Params *p, void *keys, void
   p->fast_paths = 1;
   p->mitigation = 1;
   p->dran = 1.0;
-  p->small_t = kSmallHuge;
-  p->sq_lim[0] = kSmallT;
-  p->sq_lim[1] = kSmallHuge;
-  p->sq_lim[2] = kSmallHuge;
+  p->small_t = kSmallMax - kSmallSlack;
+  p->sq_lim[0] = kSmallT - kSmallSlack;
+  p->sq_lim[1] = kSmallMax - kSmallSlack;
+  p->sq_lim[2] = kSmallMax - kSmallSlack;
   p->reproducible = 0;
 }
 

@@ -23,8 +23,12 @@ constexpr int kThreads = 256;        // every kernel: 8 warps per CTA
 constexpr int kSmallT = 4096;        // on-chip sort, 256-thread class (<= this)
 constexpr int kSmallMax = 8192;      // on-chip sort, 512-thread class, 8-byte items
 constexpr int kSmallHuge = 16384;    // on-chip sort, 512-thread class, 4-byte keys only
-constexpr int kSmallGiant = 32768;   // on-chip sort, 1024-thread class, 4-byte keys only
+#ifndef TSQ_S2_SLOTS
+#define TSQ_S2_SLOTS 40960
+#endif
+constexpr int kSmallGiant = TSQ_S2_SLOTS;   // on-chip sort, class 2 of bare 4-byte keys
 constexpr int kSmallClasses = 3;
+constexpr int kSmallSlack = 8;       // a class of S item slots takes segments of <= S - 8 keys
 constexpr int kMaxSample = 1023;     // pivot sample size cap (2^10 - 1)
 constexpr int kRunChunk = 8192;      // elements per retire work item
 constexpr int kMaxLevels = 512;      // hard stop for the level loop (never reached: the

@@ -23,8 +23,9 @@ pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
 
-SIZES32 = [4095, 4096, 4097, 5000, 8191, 8192, 8193, 12288, 16385, 32768, 65536, 200003]
-SIZES64 = [4095, 4096, 4097, 8192, 12000, 16385, 40000]
+SIZES32 = [4087, 4088, 4089, 4095, 4096, 4097, 5000, 8183, 8184, 8185, 8191, 8192, 8193, 12288,
+           16375, 16376, 16377, 16385, 32759, 32760, 32761, 32768, 65536, 200003]
+SIZES64 = [4087, 4088, 4089, 4096, 4097, 8183, 8184, 8185, 8192, 12000, 16376, 16377, 16385, 40000]
 
 
 def _shapes(n, rng, dtype):
@@ -104,9 +105,12 @@ def test_onchip_float_total_order(sorter, dtype):
 def test_onchip_whole_array_in_one_segment(sorter):
     """n <= the on-chip cut: the root segment goes straight on chip."""
     rng = np.random.default_rng(5)
-    for n in (2, 4096, 4097, 6000, 8192):
+    for n in (2, 4088, 4089, 4096, 4097, 6000, 8184):
         st = _check(rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32), sorter)
         assert st.gpu["levels"] == 0
+    # (a class of S item slots takes segments of up to S - 8 keys)
+    st = _check(rng.integers(-2**31, 2**31, 8185, dtype=np.int64).astype(np.int32), sorter)
+    assert st.gpu["levels"] == 1
 
 
 @pytest.mark.parametrize("n", [16383, 16384, 16385, 20000, 32767, 32768, 32769, 100000])
