@@ -85,6 +85,12 @@ __device__ __forceinline__ void warp_minmax(U &mn, U &mx) {
 #ifndef TSQ_S_ALIAS
 #define TSQ_S_ALIAS 0  // class 2 of bare 4-byte keys: the counters overlay the item buffer
 #endif
+#ifndef TSQ_S_TRUNC
+#define TSQ_S_TRUNC 1  // wide ranges: leading bits first, then exchange rounds
+#endif
+#ifndef TSQ_S_TPASS6
+#define TSQ_S_TPASS6 4 // leading-bit passes of a 6-bit class
+#endif
 #ifndef TSQ_S_QUAD
 #define TSQ_S_QUAD 0   // four counters per step, ranks kept from the count sweep
 #endif
@@ -319,29 +325,50 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
   // this thread's slots: slot(t*kpt + k) = slot(t*kpt) + k
   T *mine = buf + slot(tid * kpt);
   uint16_t *imine = ibuf + slot(tid * kpt);
-#ifdef TSQ_S_MAXPASS   // timing experiments only: the output is not sorted
-  const int passes0 = (bits + F::DBMAX - 1) / F::DBMAX;
-  const int passes = passes0 < TSQ_S_MAXPASS ? passes0 : TSQ_S_MAXPASS;
-  const int db = (bits + passes0 - 1) / passes0;
-#else
-  const int passes = (bits + F::DBMAX - 1) / F::DBMAX;   // bits >= 1
-  const int db = (bits + passes - 1) / passes;
-#endif
-  const uint32_t mask = (1u << db) - 1u;
-  const int R = 1 << db;
-  const int wbits = b0 + passes * db;
-  const T padv = wbits >= (int)(8 * sizeof(T)) ? ~T(0) : (T)((T(1) << wbits) - 1);
   T it[KPT];
   uint16_t ix[IDX ? KPT : 1];
   uint32_t lr[QUAD ? KPT / 4 : 1];   // each item's rank among the thread's items of its digit
   static_assert(KPT <= 256 && KPT % 8 == 0, "8-bit ranks inside a thread");
   static_assert(!ALIAS || (!QUAD && !LIN && !IDX && sizeof(T) == 4), "overlay: plain 32-bit items only");
+  // A wide range (float64 keys: ~45 bits in an 8K-key segment of 2^26 normal
+  // keys) is first sorted on its leading TB bits only -- TPASS digit passes
+  // instead of ceil(bits / DB) -- which leaves only items with equal leading
+  // bits possibly out of order: for keys spread over the range, a few
+  // adjacent pairs.  Odd-even exchange rounds over the full items put them
+  // right; if they have not settled after kFixRounds (keys clustered inside
+  // few leading-bit buckets), the full LSD passes run after all.
+#ifdef TSQ_S_TPASS
+  constexpr int TPASS = TSQ_S_TPASS;
+#else
+  constexpr int TPASS = F::DBMAX >= 6 ? TSQ_S_TPASS6 : (F::DBMAX == 5 ? 3 : 4);
+#endif
+  constexpr int TB = TPASS * F::DBMAX;
+  constexpr int kFixRounds = 12;
+  const bool trunc = TSQ_S_TRUNC && !LIN && bits > TB;
+#pragma unroll 1
+  for (int attempt = 0; attempt < 2; ++attempt) {
+  const bool tr = trunc && attempt == 0;
+  const int tbits = tr ? TB : bits;          // key bits this attempt's passes cover
+  const int shift0 = bits - tbits;
+#ifdef TSQ_S_MAXPASS   // timing experiments only: the output is not sorted
+  const int passes0 = (tbits + F::DBMAX - 1) / F::DBMAX;
+  const int passes = passes0 < TSQ_S_MAXPASS ? passes0 : TSQ_S_MAXPASS;
+  const int db = (tbits + passes0 - 1) / passes0;
+#else
+  const int passes = (tbits + F::DBMAX - 1) / F::DBMAX;   // bits >= 1
+  const int db = (tbits + passes - 1) / passes;
+#endif
+  const uint32_t mask = (1u << db) - 1u;
+  const int R = 1 << db;
+  const int wbits = b0 + passes * db;
+  const T padv = wbits >= (int)(8 * sizeof(T)) ? ~T(0) : (T)((T(1) << wbits) - 1);
 #pragma unroll 1
   for (int ps = 0; ps < passes; ++ps) {
-    const int sh = b0 + db * ps;
-    const bool last = ps == passes - 1;
-    if (ps > 0 || !LIN) __syncthreads();   // previous scatter (or the key load) complete
-    if (ps == 0) {
+    const int sh = b0 + shift0 + db * ps;
+    const bool last = ps == passes - 1 && !tr;
+    const bool first = ps == 0 && attempt == 0;
+    if (!first || !LIN) __syncthreads();   // previous scatter (or the key load) complete
+    if (first) {
       if constexpr (LIN) {
         // items from the keys in registers; a pad (all-ones key) clamps to padv
         const U padu = (U)padv;
@@ -375,7 +402,7 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
         }
       }
     }
-    if (ALIAS && !(ps == 0 && (sizeof(U) > sizeof(T) || LIN))) __syncthreads();   // every item is in registers
+    if (ALIAS && !(first && (sizeof(U) > sizeof(T) || LIN))) __syncthreads();   // every item is in registers
     {
       uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
       const int n4 = R * NT / 8;
@@ -509,6 +536,35 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
         }
       }
     }
+  }
+  if (!tr) break;
+  // odd-even exchange rounds over the full items (slots [0, len))
+  __syncthreads();
+  bool settled = false;
+#pragma unroll 1
+  for (int round = 0; round < kFixRounds && !settled; ++round) {
+    bool swapped = false;
+#pragma unroll
+    for (int ph = 0; ph < 2; ++ph) {
+      for (int i = 2 * tid + ph; i + 1 < len; i += 2 * NT) {
+        const int sa = slot(i), sb = slot(i + 1);
+        const T a = buf[sa], b = buf[sb];
+        if (a > b) {
+          buf[sa] = b;
+          buf[sb] = a;
+          if (IDX) {
+            const uint16_t ia = ibuf[sa];
+            ibuf[sa] = ibuf[sb];
+            ibuf[sb] = ia;
+          }
+          swapped = true;
+        }
+      }
+      __syncthreads();
+    }
+    settled = !__syncthreads_or(swapped);
+  }
+  if (settled) break;
   }
   U *dst = E.dst() + sm.begin;
   if constexpr (LOUT) {

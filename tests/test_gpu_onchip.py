@@ -189,6 +189,47 @@ def test_onchip_records_item_forms(sorter, dtype, n):
         assert_records_consistent(keys, dk.cpu().numpy(), dp.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.float32, np.int64, np.uint64, np.float64])
+@pytest.mark.parametrize("n", [2000, 8184, 16376, 40952])
+def test_onchip_leading_bits_then_exchange(sorter, dtype, n):
+    """A wide key range is sorted on its leading bits first and finished by
+    odd-even exchange rounds; keys clustered inside a few leading-bit buckets
+    (two outliers stretch the range, everything else differs in the low bits
+    only) do not settle in the bounded rounds and take the full radix passes.
+    Shapes: spread keys (few ties), one tight cluster, many small clusters,
+    clusters of equal keys -- keys only and records, one on-chip segment each."""
+    from conftest import assert_records_consistent
+    rng = np.random.default_rng(n * 3 + 1)
+    dt = np.dtype(dtype)
+    if dt.kind == "f":
+        spread = rng.standard_normal(n)
+        cluster = 1.0 + rng.integers(0, 1 << 20, n) * np.finfo(dt).eps
+        cluster[0], cluster[1] = -1e30, 1e30
+        # (+ 0.0: no -0.0, which the reference's comparator cannot order)
+        many = np.round(rng.standard_normal(n), 1) + 0.0 + rng.integers(0, 64, n) * np.finfo(dt).eps
+        equal = np.round(rng.standard_normal(n), 1) + 0.0
+    else:
+        info = np.iinfo(dt)
+        spread = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        mid = info.max // 2
+        cluster = (mid + rng.integers(0, 1 << 12, n)).astype(dt)
+        cluster[0], cluster[1] = info.min, info.max
+        centres = rng.integers(info.min // 2, info.max // 2, 40, dtype=np.int64 if dt.kind == "i" else np.uint64)
+        many = (centres[rng.integers(0, 40, n)] + rng.integers(0, 256, n).astype(centres.dtype)).astype(dt)
+        equal = centres[rng.integers(0, 40, n)].astype(dt)
+    for keys in (spread, cluster, many, equal):
+        keys = np.ascontiguousarray(keys.astype(dt))
+        _check(keys, sorter)
+        if n <= 16376:
+            pay = np.arange(n, dtype=np.uint32)
+            dk = torch.from_numpy(keys.copy()).cuda()
+            dp = torch.from_numpy(pay).cuda()
+            sorter.sort(T.Records(dk, dp))
+            want = keys.copy()
+            O.sort(want, seed=1, threads=4)
+            assert_records_consistent(keys, dk.cpu().numpy(), dp.cpu().numpy(), want)
+
+
 def test_verification_tiles_after_partition_tiles(cuda_ok):
     """Regression: a level whose CTAs see a partition tile followed by many
     verification tiles (sorted / reversed fast paths) -- a small random
