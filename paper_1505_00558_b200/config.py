@@ -55,8 +55,8 @@ class GpuConfig:
                  reference's _range always finishes, core.py:1643-1728);
                  0 = max(24, 2 * ceil(log2 n)).
     small_threshold  segments of at most this many keys finish in the on-chip
-                 sort; 0 = the measured default (4-byte keys 32768 -- 8192 up
-                 to 2^21 keys --, records and 8-byte keys 8192); values above
+                 sort; 0 = the measured default (4-byte keys 40952 -- 8184 up
+                 to 2^21 keys --, records and 8-byte keys 8184); values above
                  the key type's on-chip capacity are clamped to it
                  (lower it to drive the partition machine on tiny inputs, like
                  the reference tests' insertion_threshold=3)
@@ -79,8 +79,8 @@ class GpuConfig:
     reproducible: bool = False
 
     def __post_init__(self):
-        if not (self.small_threshold == 0 or 1 <= self.small_threshold <= 32768):
-            raise ValueError("small_threshold must be 0 (auto) or in [1, 32768]")
+        if not (self.small_threshold == 0 or 1 <= self.small_threshold <= 40952):
+            raise ValueError("small_threshold must be 0 (auto) or in [1, 40952]")
         if not (self.max_depth == 0 or 2 <= self.max_depth <= 190):
             raise ValueError("max_depth must be 0 (auto) or in [2, 190]")
 

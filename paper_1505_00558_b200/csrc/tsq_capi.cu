@@ -34,18 +34,17 @@ struct KernelSet {
 int key_bytes_of(int dt);
 
 // Default on-chip cut (measured on B200, scripts/cut_sweep.py, profiles/r02*):
-// 4-byte keys 32768 above 2^21 keys (uniform int32 2^26: 2.03 ms at 32768,
-// 2.04 at 16384, 2.20 at 12288; 2^24: 0.66 / 0.70 / 0.76 ms) -- a radix
-// pass over one more key bit costs less than the partition level it saves;
-// 8192 up to 2^21 keys, where fewer, larger segments would leave SMs idle.
-// Records and 8-byte keys 8192: their 1024-thread class runs at one CTA per
-// SM and f64 segments need ~9 digit passes (normal f64 2^26: 4.85 ms at
-// 8192, 4.98 at 16384; records 2^27: 9.79 / 9.90 ms).
+// bare 4-byte keys 40952 = the largest class (uniform int32 2^26: 1.87 ms
+// against 1.94 at 32760; 2^24: 0.64 / 0.68 / 0.72 at 16376; 2^20: 0.208 /
+// 0.208 / 0.222 / 0.230 at 8184) -- a radix pass over one more key bit costs
+// less than the partition level it saves, at every size.  Records and
+// 8-byte keys 8184: their largest class runs at one CTA per SM (normal f64
+// 2^26: 3.98 ms at 8184, 4.00 at 16376; records 2^27: 9.79 / 9.90 ms).
+// (A class of S item slots takes segments of <= S - kSmallSlack keys.)
 int default_small_t(int kt, int pt, size_t n) {
+  (void)n;
   const bool pay = pt == TSQ_U32;
-  // (a class of S item slots takes segments of <= S - kSmallSlack keys)
-  if (key_bytes_of(kt) == 4 && !pay)
-    return (n <= (1u << 21) ? kSmallMax : kSmallGiant) - kSmallSlack;
+  if (key_bytes_of(kt) == 4 && !pay) return kSmallGiant - kSmallSlack;
   return kSmallMax - kSmallSlack;
 }
 

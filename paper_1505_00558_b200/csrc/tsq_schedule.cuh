@@ -734,10 +734,20 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
     else atomicAdd(dst[threadIdx.x], st[threadIdx.x]);
   }
   if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t d = atomicAdd(&ctl->ctas_done, 1u);
+    // one acquire-release counter bump per CTA (after the CTA barrier above
+    // it publishes every thread's queue writes and, for the CTA that finds
+    // itself last, makes all the others' visible)
+    uint32_t d;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(d)
+                 : "l"(&ctl->ctas_done)
+                 : "memory");
     if (d == gridDim.x - 1) {
-      __threadfence();
+      // the queue state the decision needs, read side by side with the
+      // exchange of the append cursor
+      const uint32_t err0 = ld_volatile32(&ctl->error);
+      const u64 runp = ld_volatile(&ctl->run_packed);
+      const uint32_t sq0 = ld_volatile32(&ctl->sq_count[0]);
       const u64 packed = atomicExch(&ctl->next_packed, 0ull);
       const uint32_t ns = (uint32_t)(packed >> 32), nt = (uint32_t)packed;
       ctl->cur_nseg = ns;
@@ -747,20 +757,21 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
       ctl->level = level + 1;
       ctl->levels += 1;
       bool more = ns > 0;
+      uint32_t err = err0;
       if (more && level + 1 >= (uint32_t)kMaxLevels) {
         atomicOr(&ctl->error, (uint32_t)ERR_LEVELS);
-        more = false;
+        err |= (uint32_t)ERR_LEVELS;
       }
-      if (ctl->error) more = false;
+      if (err) more = false;
       // drain the on-chip and run queues before a level could overflow them:
       // one level appends at most 2 * seg_cap small segments and seg_cap runs
       // (the large on-chip class cannot overflow: its segments are disjoint
       // and longer than the small class's capacity, sq_cap[1] > n / that)
-      const uint32_t runs = (uint32_t)(ctl->run_packed >> 32);
-      const bool flush = more && (ctl->sq_count[0] + 2u * P->seg_cap > P->sq_cap[0] ||
+      const uint32_t runs = (uint32_t)(runp >> 32);
+      const bool flush = more && (sq0 + 2u * P->seg_cap > P->sq_cap[0] ||
                                   runs + P->seg_cap > P->run_cap);
       ctl->flush = flush ? 1u : 0u;
-      __threadfence();
+      // (the kernel boundary orders these writes before the next kernel)
       if (P->use_cond) cudaGraphSetConditional(P->cond, (more && !flush) ? 1u : 0u);
     }
   }

@@ -12,7 +12,9 @@ import workloads as W
 
 specs = sys.argv[1:] or ["uniform:67108864"]
 for spec in specs:
-    cuts = (8192, 12288, 16384) if spec.startswith('records') else (8192, 12288, 16384, 24576, 32768)
+    cuts = (8184, 12288, 16376) if spec.startswith("records") else (4088, 8184, 12288, 16376, 24576, 32760, 40952)
+    if os.environ.get("TSQ_CUTS"):
+        cuts = tuple(int(c) for c in os.environ["TSQ_CUTS"].split(","))
     fam, n = spec.split(":")
     n = int(n)
     keys, pay = W.generate(fam, n)

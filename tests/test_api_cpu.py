@@ -86,7 +86,7 @@ def test_sortconfig_validation_matches_reference():
         T.SortConfig(late_swap_byte_threshold=0)
     T.SortConfig(insertion_threshold=3)
     with pytest.raises(ValueError):
-        T.GpuConfig(small_threshold=32769)
+        T.GpuConfig(small_threshold=40953)
     with pytest.raises(ValueError):
         T.GpuConfig(small_threshold=-1)
     assert T.GpuConfig().small_threshold == 0  # auto: the measured per-type default

@@ -105,20 +105,23 @@ def test_onchip_float_total_order(sorter, dtype):
 def test_onchip_whole_array_in_one_segment(sorter):
     """n <= the on-chip cut: the root segment goes straight on chip."""
     rng = np.random.default_rng(5)
-    for n in (2, 4088, 4089, 4096, 4097, 6000, 8184):
+    for n in (2, 4088, 4089, 4096, 4097, 6000, 8184, 8185, 16376, 16377, 40952):
         st = _check(rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32), sorter)
         assert st.gpu["levels"] == 0
     # (a class of S item slots takes segments of up to S - 8 keys)
-    st = _check(rng.integers(-2**31, 2**31, 8185, dtype=np.int64).astype(np.int32), sorter)
+    st = _check(rng.integers(-2**31, 2**31, 40953, dtype=np.int64).astype(np.int32), sorter)
     assert st.gpu["levels"] == 1
+    for n, lv in ((8184, 0), (8185, 1)):
+        st = _check(rng.integers(-2**62, 2**62, n, dtype=np.int64), sorter)
+        assert st.gpu["levels"] == lv
 
 
-@pytest.mark.parametrize("n", [16383, 16384, 16385, 20000, 32767, 32768, 32769, 100000])
+@pytest.mark.parametrize("n", [16376, 16377, 16385, 20000, 32767, 32768, 32769, 40951, 40952, 40953, 100000])
 @pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.float32])
 def test_onchip_1024_thread_class(n, dtype, cuda_ok):
-    """The 1024-thread class (16385 .. 32768 four-byte keys): forced with
-    small_threshold=32768 at sizes around both of its boundaries."""
-    s = T.Sorter(seed=5, gpu=T.GpuConfig(small_threshold=32768))
+    """The largest class (16377 .. 40952 four-byte keys): small_threshold at
+    its capacity, sizes around both of its boundaries."""
+    s = T.Sorter(seed=5, gpu=T.GpuConfig(small_threshold=40952))
     rng = np.random.default_rng(n * 3 + 2)
     for name, x in _shapes(n, rng, dtype).items():
         _check(x, s)
