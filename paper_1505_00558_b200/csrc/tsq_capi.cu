@@ -37,14 +37,15 @@ int key_bytes_of(int dt);
 // bare 4-byte keys 40952 = the largest class (uniform int32 2^26: 1.87 ms
 // against 1.94 at 32760; 2^24: 0.64 / 0.68 / 0.72 at 16376; 2^20: 0.208 /
 // 0.208 / 0.222 / 0.230 at 8184) -- a radix pass over one more key bit costs
-// less than the partition level it saves, at every size.  Records and
-// 8-byte keys 8184: their largest class runs at one CTA per SM (normal f64
-// 2^26: 3.98 ms at 8184, 4.00 at 16376; records 2^27: 9.79 / 9.90 ms).
+// less than the partition level it saves, at every size.  Bare 8-byte keys
+// 16376, their largest class too (normal f64 2^26: 3.67 ms against 3.98 at
+// 8184).  Records 8184: their largest class runs 1024 threads at one CTA
+// per SM (records 2^27: 9.79 ms at 8192, 9.90 at 16384).
 // (A class of S item slots takes segments of <= S - kSmallSlack keys.)
 int default_small_t(int kt, int pt, size_t n) {
   (void)n;
   const bool pay = pt == TSQ_U32;
-  if (key_bytes_of(kt) == 4 && !pay) return kSmallGiant - kSmallSlack;
+  if (!pay) return (key_bytes_of(kt) == 4 ? kSmallGiant : kSmallHuge) - kSmallSlack;
   return kSmallMax - kSmallSlack;
 }
 

@@ -88,20 +88,36 @@ __device__ __forceinline__ void warp_minmax(U &mn, U &mx) {
 #ifndef TSQ_S_TRUNC
 #define TSQ_S_TRUNC 1  // wide ranges: leading bits first, then exchange rounds
 #endif
+#ifndef TSQ_S_TPASS6W
+#define TSQ_S_TPASS6W 3 // same, 8-byte keys
+#endif
 #ifndef TSQ_S_TPASS6
 #define TSQ_S_TPASS6 4 // leading-bit passes of a 6-bit class
 #endif
 #ifndef TSQ_S_QUAD
 #define TSQ_S_QUAD 0   // four counters per step, ranks kept from the count sweep
 #endif
+#ifndef TSQ_S2P_NT
+#define TSQ_S2P_NT 1024   // class 2 of records
+#endif
+#ifndef TSQ_S2P_DB
+#define TSQ_S2P_DB 5
+#endif
+#ifndef TSQ_S2W_NT
+#define TSQ_S2W_NT 512    // class 2 of bare 8-byte keys
+#endif
+#ifndef TSQ_S2W_DB
+#define TSQ_S2W_DB 6
+#endif
 template <int KB, bool PAY, int CLS>
 struct SmallClass {
   static constexpr bool BARE4 = KB == 4 && !PAY;
-  static constexpr int NT = CLS == 0 ? kThreads : (CLS == 1 ? 2 * kThreads : (BARE4 ? TSQ_S2_NT : 4 * kThreads));
+  static constexpr bool BARE8 = KB == 8 && !PAY;
+  static constexpr int NT = CLS == 0 ? kThreads : (CLS == 1 ? 2 * kThreads : (BARE4 ? TSQ_S2_NT : (BARE8 ? TSQ_S2W_NT : TSQ_S2P_NT)));
   static constexpr int SLOTS = CLS == 0   ? kSmallT
                                : CLS == 1 ? (BARE4 ? kSmallHuge : kSmallMax)
                                           : (BARE4 ? kSmallGiant : kSmallHuge);
-  static constexpr int DB = (CLS == 2 && BARE4) ? TSQ_S2_DB : 5;
+  static constexpr int DB = (CLS == 2 && BARE4) ? TSQ_S2_DB : ((CLS == 2 && BARE8) ? TSQ_S2W_DB : (CLS == 2 ? TSQ_S2P_DB : 5));
   static constexpr int MINB = CLS == 0 ? 4 : (CLS == 1 ? 2 : 1);
   // the counters overlay the item buffer: the items stay in registers from
   // the pass's first read to its scatter, the ranks are taken into registers
@@ -340,7 +356,7 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
 #ifdef TSQ_S_TPASS
   constexpr int TPASS = TSQ_S_TPASS;
 #else
-  constexpr int TPASS = F::DBMAX >= 6 ? TSQ_S_TPASS6 : (F::DBMAX == 5 ? 3 : 4);
+  constexpr int TPASS = F::DBMAX >= 6 ? (sizeof(U) == 8 ? TSQ_S_TPASS6W : TSQ_S_TPASS6) : (F::DBMAX == 5 ? 3 : 4);
 #endif
   constexpr int TB = TPASS * F::DBMAX;
   constexpr int kFixRounds = 12;

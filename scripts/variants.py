@@ -67,7 +67,7 @@ print(json.dumps({{"ms": sorted(ms[2:])[len(ms[2:]) // 2], "min": min(ms[2:]), "
     env = dict(os.environ, TSQ_LIB=lib)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     if r.returncode != 0:
-        return {"error": r.stderr[-400:]}
+        return {"error": r.stderr[-1500:]}
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 

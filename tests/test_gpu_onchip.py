@@ -111,7 +111,7 @@ def test_onchip_whole_array_in_one_segment(sorter):
     # (a class of S item slots takes segments of up to S - 8 keys)
     st = _check(rng.integers(-2**31, 2**31, 40953, dtype=np.int64).astype(np.int32), sorter)
     assert st.gpu["levels"] == 1
-    for n, lv in ((8184, 0), (8185, 1)):
+    for n, lv in ((8184, 0), (8185, 0), (16376, 0), (16377, 1)):
         st = _check(rng.integers(-2**62, 2**62, n, dtype=np.int64), sorter)
         assert st.gpu["levels"] == lv
 
