@@ -104,10 +104,9 @@ typedef struct {
                             * their key bounds (no sampling), which ends the recursion
                             * within key-bits more levels; 0 = max(24, 2 log2 n) */
   int32_t host_levels;     /* 1 = drive levels from the host (debug/per-level stats) */
-  int32_t small_threshold; /* segments <= this go on chip (1..16384); 0 = the default:
-                            * 4-byte keys 16384 (8192 up to 2^21 keys; records 8192),
-                            * 8-byte keys and records 8192; clamped to the key type's
-                            * capacity */
+  int32_t small_threshold; /* segments <= this go on chip (1..40952); 0 = the default:
+                            * bare 4-byte keys 40952, bare 8-byte keys 16376, records
+                            * 8184; clamped to the key type's on-chip capacity */
   int32_t reproducible;    /* 1 = run-to-run identical layout (decoupled look-back);
                             * 0 = tiles reserve output ranges with one atomic (faster) */
   int32_t stage_export;    /* 1 = host-driven levels with on_level called per level */
