@@ -7,38 +7,41 @@
 // between two ancestor pivots, so their encoded range is narrow (uniform int32
 // at 2^26: ~21 bits for a 32K-key segment).  One CTA per segment:
 //
-//   1. the segment arrives in shared memory -- bare keys: one bulk copy
-//      (cp.async.bulk, mbarrier) of the 16-byte aligned window around it,
-//      read back by every thread as 16-byte vectors (its chunks taken in a
-//      rotated order, so a quarter warp touches eight bank groups); records:
-//      coalesced loads -- and the CTA takes the min / max of the encoded keys;
-//      every thread forms items = key - min for its consecutive positions
-//      (records: the local index packed below it while both fit, else in a
-//      16-bit side array);
-//   2. ceil(bits(range) / DB) stable counting passes of <= DB-bit digits, each:
+//   1. coalesced load into shared memory, encode, CTA-wide min / max; the
+//      active threads (ceil(len / KPT)) read KPT consecutive keys each back
+//      ("blocked") and form items = key - min (records: the local index
+//      packed below it while both fit, else in a 16-bit side array);
+//   2. stable counting passes of <= DB-bit digits, each:
 //        count  every thread bumps its own 16-bit counter (digit, thread) for
-//               each of its items, in position order, two items per step
-//               (both counters loaded before either is stored back);
+//               each of its items, in position order;
 //        scan   one exclusive scan over the counters in (digit, thread) order
 //               gives every (digit, thread) its first output slot;
 //        rank   the same sweep again now hands out slots: each item goes to
 //               its slot in shared memory; the next pass reads them back
 //               blocked.
 //      Thread order = position order inside a digit, so every pass is stable
-//      and the LSD passes leave the items in key order.
-//   3. bare keys: the last pass scatters the decoded keys (min + item) into a
-//      linear image of the destination window, which leaves as bulk copies
-//      (ragged ends as scalar stores); records: keys written back coalesced,
-//      payloads gathered by local index.
+//      and the LSD passes leave the items in key order.  A range wider than
+//      TPASS * DB bits is sorted on its leading bits only, then finished by
+//      odd-even exchange rounds over the full items (radix_run);
+//   3. keys written back as min + item (caller's encoding, coalesced);
+//      record payloads gathered by local index.
 //
-// Measured alternatives (B200, uniform int32 2^26, profiles/r02*): warp-
-// collective ranking with __match_any_sync runs on the ADU pipe at ~2
-// SM-cycles per distinct digit in the warp (60 per 8-bit match,
-// scripts/micro/match_tp.cu) -- 2.3 ms for the on-chip sort; ballot-based
-// peer masks take ~9 instructions per digit bit; shared-memory atomics run at
-// 2 cycles per lane.  The round-1 warp bitonic + merge-path sort took 0.95 ms
-// at ~320 instructions per key; 1024 threads x 32 keys with 5-bit digits
-// 0.68 ms at ~176 (70 % of the shared-memory wavefront peak).
+// Measured alternatives (B200, uniform int32 2^26, DESIGN.md section 9;
+// several are still here behind the TSQ_S_* switches): warp-collective
+// ranking with __match_any_sync runs on the ADU pipe at ~2 SM-cycles per
+// distinct digit in the warp (60 per 8-bit match, scripts/micro/match_tp.cu)
+// -- 2.3 ms for the on-chip sort; ballot-based peer masks take ~9
+// instructions per digit bit; shared-memory atomics run at 2 cycles per lane;
+// 256 threads x 128 keys with 7-bit digits cannot hide the counter
+// read-modify-write chain (8 warps per SM); the segment brought in by bulk
+// copy and read as 16-byte chunks costs more instructions than the coalesced
+// loads it replaces; paired / quad counter steps with kept ranks add more
+// instructions than the latency they hide at 16 warps; counters overlaying
+// the item buffer (7-bit digits at 512 threads) double the zero + scan work.
+// The round-1 warp bitonic + merge-path sort took 0.95 ms at ~320
+// instructions per key; 1024 threads x 32 keys with 5-bit digits 0.68 ms at
+// ~176; this geometry (512 x 80, 6-bit digits, 40960 slots) 0.59 ms at ~130,
+// shared-memory wavefronts at 62 % of peak.
 #pragma once
 
 #include "tsq_bitonic.cuh"
@@ -564,6 +567,7 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
     for (int ph = 0; ph < 2; ++ph) {
       for (int i = 2 * tid + ph; i + 1 < len; i += 2 * NT) {
         const int sa = slot(i), sb = slot(i + 1);
+        TSQ_CHECK(sa >= 0 && sb < F::CAPP);
         const T a = buf[sa], b = buf[sb];
         if (a > b) {
           buf[sa] = b;

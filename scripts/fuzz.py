@@ -76,7 +76,7 @@ for c in range(cases):
     if os.environ.get("TSQ_FUZZ_BIG") == "1":  # large inputs: 2^22 .. 2^25 keys
         n = int(rng.integers(1 << 22, 1 << 25))
     x, kind = keys_of(dt, n)
-    thr = int(rng.choice([0, 0, 0, 1, 3, 16, 4096, 8192, 16384, 24576, 32768]))
+    thr = int(rng.choice([0, 0, 0, 1, 3, 16, 4088, 4096, 8184, 8192, 16376, 16384, 24576, 32768, 40952]))
     if os.environ.get("TSQ_FUZZ_TINY") == "1":  # stress: the partition machine down to tiny segments
         thr = int(rng.choice([1, 2, 3]))
     rep = bool(rng.integers(0, 2))
