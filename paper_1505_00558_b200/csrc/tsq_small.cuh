@@ -97,6 +97,9 @@ __device__ __forceinline__ void warp_minmax(U &mn, U &mx) {
 #ifndef TSQ_S_TPASS6
 #define TSQ_S_TPASS6 4 // leading-bit passes of a 6-bit class
 #endif
+#ifndef TSQ_S_PREFETCH
+#define TSQ_S_PREFETCH 1  // the next segment's keys prefetched into L2 during the current sort
+#endif
 #ifndef TSQ_S_QUAD
 #define TSQ_S_QUAD 0   // four counters per step, ranks kept from the count sweep
 #endif
@@ -653,9 +656,10 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
 
 // Sort one queued segment (all threads of the CTA).  `phase`: parity of the
 // load barrier's next completion.
-template <class C, bool PAY, int CLS>
+template <class C, bool PAY, int CLS, class AfterLoad>
 __device__ __forceinline__ void radix_sort_seg(const SmallEnv<typename C::U> &E, const SmallSeg &sm,
-                                               unsigned char *smem, uint32_t &phase) {
+                                               unsigned char *smem, uint32_t &phase,
+                                               AfterLoad after_load) {
   typedef typename C::U U;
   typedef RadixGeo<C, PAY, CLS> G;
   constexpr int KPT = G::KPT, NW = G::NW, NT = G::NT, VN = G::VN;
@@ -744,7 +748,11 @@ __device__ __forceinline__ void radix_sort_seg(const SmallEnv<typename C::U> &E,
     // shared array and would be serialised)
     const SlotMap<KPT, false> slot(KPT);
     U *kbuf = reinterpret_cast<U *>(smem + 1024);
+#ifdef TSQ_S_LB
+    constexpr int LB = (KPT % TSQ_S_LB == 0 && KPT >= 64) ? TSQ_S_LB : ((sizeof(U) == 8 || KPT < 16) ? 8 : 16);
+#else
     constexpr int LB = (sizeof(U) == 8 || KPT < 16) ? 8 : 16;   // loads in flight per batch
+#endif
 #pragma unroll 1
     for (int q0 = 0; q0 < KPT; q0 += LB) {
       if (q0 * NT >= len) break;
@@ -773,6 +781,7 @@ __device__ __forceinline__ void radix_sort_seg(const SmallEnv<typename C::U> &E,
     s_mm[NW + warp] = mx;
   }
   __syncthreads();
+  after_load();   // the segment's keys are on chip
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     const U a = s_mm[w], b = s_mm[NW + w];
@@ -835,16 +844,42 @@ __global__ void __launch_bounds__(RadixGeo<C, PAY, CLS>::NT, RadixGeo<C, PAY, CL
   }
   uint32_t phase = 0;
   uint64_t elems = 0;
-  for (;;) {
-    if (threadIdx.x == 0) *s_ticket = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t t = *s_ticket;
-    __syncthreads();
-    if (t >= count) break;
+  // tickets are claimed one segment ahead: while a segment is sorted, the
+  // next one's keys are on their way into L2 (bulk prefetch)
+  if (threadIdx.x == 0) *s_ticket = atomicAdd(ticket, 1u);
+  __syncthreads();
+  uint32_t t = *s_ticket;
+  while (t < count) {
     const SmallSeg sm = q[t];
-    radix_sort_seg<C, PAY, CLS>(E, sm, smem_raw, phase);
+    __syncthreads();   // everyone has read the ticket
+    if (threadIdx.x == 0) *s_ticket = atomicAdd(ticket, 1u);
+    auto prefetch_next = [&]() {
+#if TSQ_S_PREFETCH
+      if (threadIdx.x < 32) {
+        const uint32_t tn = *s_ticket;   // written before the barrier just passed
+        if (tn < count) {
+          const SmallSeg nx = q[tn];
+          const char *p0 = reinterpret_cast<const char *>(E.keys(nx.buf) + nx.begin);
+          const char *p1 = p0 + (size_t)nx.len * sizeof(U);
+          const char *a0 = reinterpret_cast<const char *>(((uintptr_t)p0 + 15) & ~(uintptr_t)15);
+          const char *a1 = reinterpret_cast<const char *>((uintptr_t)p1 & ~(uintptr_t)15);
+          if (a1 > a0) {
+            const size_t per = (((size_t)(a1 - a0) / 32) + 15) & ~(size_t)15;
+            const char *b0 = a0 + per * threadIdx.x;
+            if (b0 < a1) {
+              const size_t nb = (size_t)(a1 - b0) < per ? (size_t)(a1 - b0) : per;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((uint32_t)nb)
+                           : "memory");
+            }
+          }
+        }
+      }
+#endif
+    };
+    radix_sort_seg<C, PAY, CLS>(E, sm, smem_raw, phase, prefetch_next);
     elems += (uint64_t)sm.len;
     __syncthreads();
+    t = *s_ticket;
   }
   if (RadixGeo<C, PAY, CLS>::LIN && threadIdx.x < 32) bulk_wait0();
   if (threadIdx.x == 0 && elems) {
