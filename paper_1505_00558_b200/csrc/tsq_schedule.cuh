@@ -389,6 +389,9 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
                                     u64 *st, RoundShared &rs) {
   typedef typename C::U U;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarpQ = (kWarpSampleMax + 32) / 32;   // samples per lane (4 for 127)
+  U sv[kWarpQ];
+  int S = 0;   // > 0: this warp's child awaits its pivot (samples in sv)
   if (lane == 0) {
     rs.lv[warp][0].valid = rs.lv[warp][1].valid = 0;
     rs.sm[warp][0].valid = rs.sm[warp][1].valid = 0;
@@ -450,8 +453,14 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
           piv = bisect_pivot(klo, khi);
           if (lane == 0) atomicAdd(&st[ST_BISECTED], 1ull);
         } else {
-          piv = (u64)warp_select_pivot<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
-                                          cb, cl, P->dran, P->mitigation, &flag);
+          // the samples are only loaded here; they are sorted after the
+          // round's queue claims, whose round trip their loads overlap
+          S = sample_count(cl);
+          if (S > kWarpSampleMax) S = kWarpSampleMax;
+          __syncwarp();
+          load_samples<C, kWarpQ>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db], cb, cl, S,
+                                  P->dran, P->mitigation, lane, sv);
+          piv = 0;
         }
         if (lane == 0) {
           uint32_t kind = KIND_PARTITION;
@@ -504,6 +513,20 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     }
   }
   __syncthreads();
+  if (S > 0) {
+    // the pivot: median of the sorted samples; the order flag picks the
+    // verification fast paths
+    const int flag = warp_order_flag<U, kWarpQ>(sv, S);
+    warp_bitonic<U, kWarpQ>(sv);
+    const u64 piv = (u64)warp_pick<U, kWarpQ>(sv, S >> 1);
+    if (lane == 0) {
+      ReqLevel &q = rs.lv[warp][0];
+      q.pivot = piv;
+      if (P->fast_paths)
+        q.kind = flag > 0 ? KIND_VERIFY_ASC : (flag < 0 ? KIND_VERIFY_DESC : KIND_PARTITION);
+    }
+    __syncwarp();
+  }
   // each warp writes its records at its offsets
   uint32_t lslot = rs.lv_slot0, ltile = rs.lv_tile0, rslot = rs.run_slot0;
   uint32_t rchunk = rs.run_chunk0;

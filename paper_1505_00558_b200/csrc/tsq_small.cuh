@@ -48,6 +48,22 @@
 
 namespace tsq {
 
+// phase clocks of CTA 0 (profiling builds only: -DTSQ_S_CLOCK; printed at kernel end)
+#ifdef TSQ_S_CLOCK
+__device__ long long g_ph[16];
+__device__ long long g_ph_last;
+#define TSQ_PH(i)                                   \
+  do {                                              \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {      \
+      const long long c_ = clock64();               \
+      g_ph[i] += c_ - g_ph_last;                    \
+      g_ph_last = c_;                               \
+    }                                               \
+  } while (0)
+#else
+#define TSQ_PH(i) ((void)0)
+#endif
+
 template <typename U>
 __device__ __forceinline__ void warp_minmax(U &mn, U &mx) {
   if constexpr (sizeof(U) == 4) {
@@ -390,6 +406,7 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
     const bool last = ps == passes - 1 && !tr;
     const bool first = ps == 0 && attempt == 0;
     if (!first || !LIN) __syncthreads();   // previous scatter (or the key load) complete
+    TSQ_PH(ps == 0 ? 2 : 8);
     if (first) {
       if constexpr (LIN) {
         // items from the keys in registers; a pad (all-ones key) clamps to padv
@@ -425,12 +442,14 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
       }
     }
     if (ALIAS && !(first && (sizeof(U) > sizeof(T) || LIN))) __syncthreads();   // every item is in registers
+    TSQ_PH(first ? 3 : 4);
     {
       uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
       const int n4 = R * NT / 8;
       for (int i = tid; i < n4; i += NT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
+    TSQ_PH(5);
     // count: this thread's items, in position order, four per step: the
     // four counters are read together, each item's rank among the thread's
     // items of its digit (counter + equal digits earlier in the step) is
@@ -475,8 +494,10 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
       }
     }
     __syncthreads();
+    TSQ_PH(6);
     radix_scan<NT, F::RMAX>(cnt, wt, R);
     __syncthreads();
+    TSQ_PH(7);
     // rank + scatter: an item's slot = its (digit, thread) prefix + its rank
     // in the thread; the prefixes of eight items are read before the first
     // scatter store
@@ -621,6 +642,7 @@ __device__ __forceinline__ void radix_run(const SmallEnv<typename C::U> &E, cons
     return;
   }
   __syncthreads();
+  TSQ_PH(8);
   // buf[0, len) holds the sorted items
   const bool dst_raw = E.raw0;
   if (PAY) {
@@ -774,6 +796,7 @@ __device__ __forceinline__ void radix_sort_seg(const SmallEnv<typename C::U> &E,
       }
     }
   }
+  TSQ_PH(1);
   warp_minmax<U>(mn, mx);
   U *s_mm = reinterpret_cast<U *>(smem);
   if (lane == 0) {
@@ -842,6 +865,9 @@ __global__ void __launch_bounds__(RadixGeo<C, PAY, CLS>::NT, RadixGeo<C, PAY, CL
     mbar_init(bar, 1);
     fence_barrier_init();
   }
+#ifdef TSQ_S_CLOCK
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_ph_last = clock64();
+#endif
   uint32_t phase = 0;
   uint64_t elems = 0;
   // tickets are claimed one segment ahead: while a segment is sorted, the
@@ -852,6 +878,7 @@ __global__ void __launch_bounds__(RadixGeo<C, PAY, CLS>::NT, RadixGeo<C, PAY, CL
   while (t < count) {
     const SmallSeg sm = q[t];
     __syncthreads();   // everyone has read the ticket
+    TSQ_PH(0);
     if (threadIdx.x == 0) *s_ticket = atomicAdd(ticket, 1u);
     auto prefetch_next = [&]() {
 #if TSQ_S_PREFETCH
@@ -879,8 +906,17 @@ __global__ void __launch_bounds__(RadixGeo<C, PAY, CLS>::NT, RadixGeo<C, PAY, CL
     radix_sort_seg<C, PAY, CLS>(E, sm, smem_raw, phase, prefetch_next);
     elems += (uint64_t)sm.len;
     __syncthreads();
+    TSQ_PH(9);
     t = *s_ticket;
   }
+#ifdef TSQ_S_CLOCK
+  if (blockIdx.x == 0 && threadIdx.x == 0 && elems) {
+    printf("class %d phases (cycles, CTA 0, %llu keys): ticket %lld load %lld minmax+sync %lld items0 %lld reload %lld "
+           "zero %lld count %lld scan %lld rank+scatter %lld output %lld\n", CLS, (unsigned long long)elems,
+           g_ph[0], g_ph[1], g_ph[2], g_ph[3], g_ph[4], g_ph[5], g_ph[6], g_ph[7], g_ph[8], g_ph[9]);
+    for (int i = 0; i < 16; ++i) g_ph[i] = 0;
+  }
+#endif
   if (RadixGeo<C, PAY, CLS>::LIN && threadIdx.x < 32) bulk_wait0();
   if (threadIdx.x == 0 && elems) {
     atomicAdd(&ctl->small_elements, (u64)elems);
