@@ -301,27 +301,95 @@ __device__ __forceinline__ void load_keys(const typename C::U *sk, const uint32_
   }
 }
 
+// One key of a whole keys-only tile into its run: two compares, one
+// predicated store at the selected side's slot (a second, predicated-off
+// store per key measured 2 % slower per sort) and a predicated step per side
+// (the compiler's own code for the same
+// loop re-derives each slot address from the rank and repeats the compares,
+// ~12 instructions per key).  a_lt / a_gt: shared-window byte addresses of the
+// thread's next < slot and next > slot; s_lt / s_gt: the (signed) byte steps
+// to the slot after it.
+template <bool SIGNED>
+__device__ __forceinline__ void place_key(uint32_t &a_lt, uint32_t &a_gt, uint32_t s_lt,
+                                          uint32_t s_gt, uint32_t x, uint32_t piv, uint32_t y) {
+  if (SIGNED)
+    asm volatile(
+        "{\n\t.reg .pred pl, pg, pe;\n\t.reg .u32 a;\n\t"
+        "setp.lt.s32 pl, %2, %3;\n\tsetp.gt.s32 pg, %2, %3;\n\t"
+        "selp.u32 a, %0, %1, pl;\n\tor.pred pe, pl, pg;\n\t@pe st.shared.u32 [a], %4;\n\t"
+        "@pl add.u32 %0, %0, %5;\n\t@pg add.u32 %1, %1, %6;\n\t}"
+        : "+r"(a_lt), "+r"(a_gt)
+        : "r"(x), "r"(piv), "r"(y), "r"(s_lt), "r"(s_gt)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred pl, pg, pe;\n\t.reg .u32 a;\n\t"
+        "setp.lt.u32 pl, %2, %3;\n\tsetp.gt.u32 pg, %2, %3;\n\t"
+        "selp.u32 a, %0, %1, pl;\n\tor.pred pe, pl, pg;\n\t@pe st.shared.u32 [a], %4;\n\t"
+        "@pl add.u32 %0, %0, %5;\n\t@pg add.u32 %1, %1, %6;\n\t}"
+        : "+r"(a_lt), "+r"(a_gt)
+        : "r"(x), "r"(piv), "r"(y), "r"(s_lt), "r"(s_gt)
+        : "memory");
+}
+template <bool SIGNED>
+__device__ __forceinline__ void place_key(uint32_t &a_lt, uint32_t &a_gt, uint32_t s_lt,
+                                          uint32_t s_gt, u64 x, u64 piv, u64 y) {
+  if (SIGNED)
+    asm volatile(
+        "{\n\t.reg .pred pl, pg, pe;\n\t.reg .u32 a;\n\t"
+        "setp.lt.s64 pl, %2, %3;\n\tsetp.gt.s64 pg, %2, %3;\n\t"
+        "selp.u32 a, %0, %1, pl;\n\tor.pred pe, pl, pg;\n\t@pe st.shared.u64 [a], %4;\n\t"
+        "@pl add.u32 %0, %0, %5;\n\t@pg add.u32 %1, %1, %6;\n\t}"
+        : "+r"(a_lt), "+r"(a_gt)
+        : "l"(x), "l"(piv), "l"(y), "r"(s_lt), "r"(s_gt)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred pl, pg, pe;\n\t.reg .u32 a;\n\t"
+        "setp.lt.u64 pl, %2, %3;\n\tsetp.gt.u64 pg, %2, %3;\n\t"
+        "selp.u32 a, %0, %1, pl;\n\tor.pred pe, pl, pg;\n\t@pe st.shared.u64 [a], %4;\n\t"
+        "@pl add.u32 %0, %0, %5;\n\t@pg add.u32 %1, %1, %6;\n\t}"
+        : "+r"(a_lt), "+r"(a_gt)
+        : "l"(x), "l"(piv), "l"(y), "r"(s_lt), "r"(s_gt)
+        : "memory");
+}
+
 // Stage one consumer thread's keys back into the stage, in output order:
 // each key goes to the thread's next < slot (counting up) or next > slot
 // (counting down); records also stage the == payloads.  MODE 0: both
 // buffers hold encoded keys, 1: source raw, 2: destination raw, 3: both raw.
+// plt / pgt / peq: the thread's first < slot, first > slot (its runs' last)
+// and first == payload slot; st_lt / st_gt: slots between two consecutive
+// keys of the thread in a run (whole keys-only tiles; 1 otherwise).
 template <class C, bool PAY, bool FULL, int MODE>
 __device__ __forceinline__ void stage_keys(const typename C::U *key, const uint32_t *pay, int tid,
                                            typename C::U piv, int rlo, int rhi, uint32_t plt,
-                                           uint32_t pgt, uint32_t peq, typename C::U *ok,
-                                           uint32_t *op) {
+                                           uint32_t pgt, uint32_t peq, uint32_t st_lt,
+                                           uint32_t st_gt, typename C::U *ok, uint32_t *op) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
+  // MODE 3 with a raw-order codec: native compare against the decoded pivot
+  constexpr bool RC = MODE == 3 && C::kRawOrder;
+  constexpr bool LEAN = !PAY && FULL;
+  uint32_t a_lt = 0, a_gt = 0, s_lt = 0, s_gt = 0;
+  if (LEAN) {
+    a_lt = smem_u32(ok + plt);
+    a_gt = smem_u32(ok + pgt);
+    s_lt = st_lt * (uint32_t)sizeof(U);
+    s_gt = 0u - st_gt * (uint32_t)sizeof(U);
+  }
 #pragma unroll
   for (int v = 0; v < G::VPT; ++v) {
     const int e0 = (v * kConsumers + tid) * G::VN;
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) {
       const U kq = key[v * G::VN + q];
-      // MODE 3 with a raw-order codec: native compare against the decoded pivot
-      constexpr bool RC = MODE == 3 && C::kRawOrder;
       const U x = RC ? kq : ((MODE & 1) ? C::enc(kq) : kq);
       const U y = MODE == 2 ? C::dec(kq) : (MODE == 1 ? x : kq);
+      if (LEAN) {
+        place_key<RC && C::kSigned>(a_lt, a_gt, s_lt, s_gt, x, piv, y);
+        continue;
+      }
       const bool valid = FULL || (e0 + q >= rlo && e0 + q < rhi);
       const bool is_lt = valid && (RC ? C::rlt(x, piv) : x < piv);
       const bool is_gt = valid && (RC ? C::rlt(piv, x) : x > piv);
@@ -418,6 +486,22 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   uint32_t pgt = (uint32_t)o_gt + t_gt - 1u - w_gt - e_gt;  // next > slot (backwards)
   uint32_t peq = (uint32_t)o_eq + w_eq + (e_va - e_lt - e_gt);
   const bool full = rlo == 0 && rhi == G::TILE;
+  // A warp whose lanes all place the same number c of < keys (sorted or
+  // blockwise-sorted input: whole tiles on one side of the pivot) would store
+  // to slots c apart in every step -- gcd(c, 32)-way bank conflicts, 8-way at
+  // c = 24 (measured: such passes ran 0.125 ms against 0.094 at 2^26).  Its
+  // 32 c slots are dealt column-wise instead: lane l takes slots l, l + 32,
+  // ... of the warp's part of the run (a bijection exactly because the counts
+  // are equal; the order of a run's keys is free).  Same for the > side.
+  uint32_t st_lt = 1, st_gt = 1;
+  if (!PAY && full) {
+    const uint32_t lane = (uint32_t)tid & 31u;
+    const uint32_t wl = c.w[warp][0], wg = c.w[warp][2];
+    const bool ul = __all_sync(0xffffffffu, e_lt == (wl >> 5) * lane) && (wl & 31u) == 0;
+    const bool ug = __all_sync(0xffffffffu, e_gt == (wg >> 5) * lane) && (wg & 31u) == 0;
+    if (ul) { plt = (uint32_t)o_lt + w_lt + lane; st_lt = 32; }
+    if (ug) { pgt = (uint32_t)o_gt + t_gt - 1u - w_gt - lane; st_gt = 32; }
+  }
   named_sync(1, kConsumers);  // every consumer holds its keys: restage in place
 #if defined(TSQ_EXP_COPY) && !defined(TSQ_EXP_STAGE)
   if (full) {  // experiment: pipeline ceiling -- the tile goes out unpartitioned
@@ -437,17 +521,17 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
   if (src_raw && dst_raw) {
     // raw-order codecs compare in the caller's encoding: the decoded pivot
     const U pv3 = C::kRawOrder ? C::dec(piv) : piv;
-    if (full) TSQ_STAGE<C, PAY, true, 3>(key, pay, tid, pv3, rlo, rhi, plt, pgt, peq, sk, sp);
-    else TSQ_STAGE<C, PAY, false, 3>(key, pay, tid, pv3, rlo, rhi, plt, pgt, peq, sk, sp);
+    if (full) TSQ_STAGE<C, PAY, true, 3>(key, pay, tid, pv3, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 3>(key, pay, tid, pv3, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
   } else if (src_raw) {
-    if (full) TSQ_STAGE<C, PAY, true, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
-    else TSQ_STAGE<C, PAY, false, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    if (full) TSQ_STAGE<C, PAY, true, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 1>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
   } else if (dst_raw) {
-    if (full) TSQ_STAGE<C, PAY, true, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
-    else TSQ_STAGE<C, PAY, false, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    if (full) TSQ_STAGE<C, PAY, true, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 2>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
   } else {
-    if (full) TSQ_STAGE<C, PAY, true, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
-    else TSQ_STAGE<C, PAY, false, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, sk, sp);
+    if (full) TSQ_STAGE<C, PAY, true, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
+    else TSQ_STAGE<C, PAY, false, 0>(key, pay, tid, piv, rlo, rhi, plt, pgt, peq, st_lt, st_gt, sk, sp);
   }
 #undef TSQ_STAGE
   fence_proxy_async_smem();

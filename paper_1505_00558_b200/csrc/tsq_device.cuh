@@ -195,6 +195,7 @@ template <int DT> struct Codec;
 // keep the order-preserving unsigned encoding in the workspace buffer.
 template <> struct Codec<TSQ_I32> {
   typedef uint32_t U;
+  static constexpr bool kSigned = true;  // rlt is a signed compare
   static constexpr bool kRawOrder = true;
   static __device__ __forceinline__ bool rlt(U a, U b) { return (int32_t)a < (int32_t)b; }
   static __device__ __forceinline__ U enc(U x) { return x ^ 0x80000000u; }
@@ -202,6 +203,7 @@ template <> struct Codec<TSQ_I32> {
 };
 template <> struct Codec<TSQ_U32> {
   typedef uint32_t U;
+  static constexpr bool kSigned = false;  // rlt is a signed compare
   static constexpr bool kRawOrder = true;
   static __device__ __forceinline__ bool rlt(U a, U b) { return a < b; }
   static __device__ __forceinline__ U enc(U x) { return x; }
@@ -209,6 +211,7 @@ template <> struct Codec<TSQ_U32> {
 };
 template <> struct Codec<TSQ_F32> {
   typedef uint32_t U;
+  static constexpr bool kSigned = false;  // rlt is a signed compare
   static constexpr bool kRawOrder = false;
   static __device__ __forceinline__ bool rlt(U a, U b) { return enc(a) < enc(b); }
   static __device__ __forceinline__ U enc(U x) {
@@ -220,6 +223,7 @@ template <> struct Codec<TSQ_F32> {
 };
 template <> struct Codec<TSQ_I64> {
   typedef u64 U;
+  static constexpr bool kSigned = true;  // rlt is a signed compare
   static constexpr bool kRawOrder = true;
   static __device__ __forceinline__ bool rlt(U a, U b) { return (long long)a < (long long)b; }
   static __device__ __forceinline__ U enc(U x) { return x ^ 0x8000000000000000ull; }
@@ -227,6 +231,7 @@ template <> struct Codec<TSQ_I64> {
 };
 template <> struct Codec<TSQ_U64> {
   typedef u64 U;
+  static constexpr bool kSigned = false;  // rlt is a signed compare
   static constexpr bool kRawOrder = true;
   static __device__ __forceinline__ bool rlt(U a, U b) { return a < b; }
   static __device__ __forceinline__ U enc(U x) { return x; }
@@ -234,6 +239,7 @@ template <> struct Codec<TSQ_U64> {
 };
 template <> struct Codec<TSQ_F64> {
   typedef u64 U;
+  static constexpr bool kSigned = false;  // rlt is a signed compare
   static constexpr bool kRawOrder = false;
   static __device__ __forceinline__ bool rlt(U a, U b) { return enc(a) < enc(b); }
   static __device__ __forceinline__ U enc(U x) {

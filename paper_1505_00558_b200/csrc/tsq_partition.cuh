@@ -63,7 +63,12 @@ __device__ __forceinline__ T bcast(T v, int src) {
 // increasing tile order, so a look-back (reproducible mode) only ever waits
 // on tiles already claimed; the next chunk is claimed before the current one
 // runs out, so the claim's round trip stays off the producer's path.
-__device__ __forceinline__ uint32_t guided_chunk(uint32_t claimed, uint32_t ntiles, uint32_t grid) {
+__device__ __forceinline__ uint32_t guided_chunk(uint32_t claimed, uint32_t ntiles, uint32_t grid,
+                                                 bool single) {
+  // reproducible mode: one tile per claim -- a chunk's first tile would wait
+  // in its look-back for the whole chunk of the CTA before it (measured:
+  // 11.7 ms instead of 0.12 ms per level at 2^26 with 32-tile chunks)
+  if (single) return 1u;
   const uint32_t left = claimed < ntiles ? ntiles - claimed : 0u;
   uint32_t c = left / (4u * grid);
   return c < 1u ? 1u : (c > 32u ? 32u : c);
@@ -94,7 +99,7 @@ __device__ __forceinline__ void producer_loop(const Params *P, int cur, uint32_t
       cn = __shfl_sync(0xffffffffu, nn, 0);
       ci = 0;
       if (lane == 0 && c0 < ntiles && grid < ntiles) {
-        nn = guided_chunk(c0 + cn > grid ? c0 + cn : grid, ntiles, grid);
+        nn = guided_chunk(c0 + cn > grid ? c0 + cn : grid, ntiles, grid, P->reproducible != 0);
         n0 = grid + atomicAdd(ticket, nn);
       } else if (lane == 0) {
         n0 = ntiles;  // nothing left to claim
