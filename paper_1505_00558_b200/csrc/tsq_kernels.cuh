@@ -262,6 +262,12 @@ __global__ void __launch_bounds__(kThreads) export_level_kernel(const Params *__
   }
 }
 
+__device__ __forceinline__ uint4 reversed(const uint4 &v) { return make_uint4(v.w, v.z, v.y, v.x); }
+__device__ __forceinline__ uint2 reversed(const uint2 &v) { return make_uint2(v.y, v.x); }
+__device__ __forceinline__ ulonglong2 reversed(const ulonglong2 &v) {
+  return make_ulonglong2(v.y, v.x);
+}
+
 // Retire finished runs into buffer 0, chunk by chunk.
 constexpr int kRB = 8;  // loads in flight per thread
 
@@ -321,6 +327,41 @@ __global__ void __launch_bounds__(kThreads) retire_kernel(const Params *__restri
             if (rawb != raw0) x = rawb ? C::enc(x) : C::dec(x);
             k0[r.begin + i] = x;
             if (PAY) p0[r.begin + i] = pv[q];
+          }
+        }
+      }
+    } else if (P->aligned[0] && (r.begin & (Vec<U>::N - 1)) == 0 &&
+               (r.len & (2 * Vec<U>::N - 1)) == 0) {
+      // RUN_REVERSED in buffer 0, vector-aligned (the root of a descending
+      // input): mirror pairs of 16-byte vectors, each reversed in registers
+      constexpr int VN = Vec<U>::N;
+      typedef typename Vec<U>::K KV;
+      typedef typename Vec<U>::P PV;
+      const long long half = r.len >> 1;
+      const long long hi = (lo + kRunChunk) < half ? (lo + kRunChunk) : half;
+      KV *kv = reinterpret_cast<KV *>(k0 + r.begin);
+      PV *pvv = PAY ? reinterpret_cast<PV *>(p0 + r.begin) : nullptr;
+      const long long nv = r.len / VN;  // vectors in the run; vector j mirrors nv - 1 - j
+      constexpr int RBV = 4;
+      for (long long j0 = lo / VN + threadIdx.x; j0 < hi / VN; j0 += (long long)kThreads * RBV) {
+        KV x[RBV], y[RBV];
+        PV px[RBV], py[RBV];
+#pragma unroll
+        for (int q = 0; q < RBV; ++q) {
+          const long long j = j0 + (long long)q * kThreads;
+          if (j < hi / VN) {
+            x[q] = kv[j];
+            y[q] = kv[nv - 1 - j];
+            if (PAY) { px[q] = pvv[j]; py[q] = pvv[nv - 1 - j]; }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < RBV; ++q) {
+          const long long j = j0 + (long long)q * kThreads;
+          if (j < hi / VN) {
+            kv[j] = reversed(y[q]);
+            kv[nv - 1 - j] = reversed(x[q]);
+            if (PAY) { pvv[j] = reversed(py[q]); pvv[nv - 1 - j] = reversed(px[q]); }
           }
         }
       }

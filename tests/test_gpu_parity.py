@@ -453,3 +453,46 @@ def test_reproducible_records_payload_order(cuda_ok, keydt):
     assert outs[0][0].tobytes() == outs[1][0].tobytes() == np.sort(keys).tobytes()
     assert np.array_equal(outs[0][1], outs[1][1])
     assert_records_consistent(keys, outs[0][0], outs[0][1], np.sort(keys))
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.uint64, np.float64])
+@pytest.mark.parametrize("n", [100000, 100001, 100004, 1 << 20])
+@pytest.mark.parametrize("payload", [False, True], ids=["keys", "records"])
+def test_reversed_input_mirror_swap(cuda_ok, dtype, n, payload):
+    """A strictly descending input is verified and reversed in place
+    (_reversed_handler, core.py:1294-1556): mirror pairs of 16-byte vectors when
+    the run is vector-aligned (n a multiple of 8 / 4), single keys otherwise;
+    an offset view takes the aligned copy."""
+    x = np.arange(n, 0, -1).astype(dtype)
+    pay = np.arange(n, dtype=np.uint32)
+    for off in (0, 1):
+        dk, dp = _dev(x)[off:], _dev(pay)[off:]
+        st = T.Sorter(seed=1).sort_with_stats(T.Records(dk, dp) if payload else dk)
+        assert st.gpu["reversed_bypass"] == 1 and st.gpu["levels"] == 1
+        want = np.sort(x[off:])
+        assert dk.cpu().numpy().tobytes() == want.tobytes()
+        if payload:
+            assert np.array_equal(dp.cpu().numpy(), pay[off:][::-1])
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.int64, np.float32])
+@pytest.mark.parametrize("shape", ["ascending", "blocks", "two_runs", "organ_pipe"])
+def test_structured_tiles_equal_lane_counts(cuda_ok, dtype, shape):
+    """Inputs whose tiles fall whole on one side of the pivot (every lane of a
+    consumer warp places the same number of keys: the column-wise slot dealing
+    of the restage), with the fast paths off so that they are partitioned."""
+    n = 300000
+    rng = np.random.default_rng(5)
+    base = np.arange(n, dtype=np.int64) - n // 2
+    if shape == "blocks":
+        b = base[: n - n % 4096].reshape(-1, 4096)
+        base = np.concatenate([b[rng.permutation(b.shape[0])].reshape(-1), base[n - n % 4096:]])
+    elif shape == "two_runs":
+        base = np.concatenate([base[0::2], base[1::2]])
+    elif shape == "organ_pipe":
+        base = np.concatenate([base[0::2], base[1::2][::-1]])
+    x = (base - base.min()).astype(dtype) if np.dtype(dtype).kind == "u" else base.astype(dtype)
+    for repro in (False, True):
+        d = _dev(x)
+        T.Sorter(seed=1, gpu=T.GpuConfig(fast_paths=False, reproducible=repro)).sort(d)
+        assert d.cpu().numpy().tobytes() == np.sort(x).tobytes()
