@@ -285,9 +285,12 @@ LevelLaunch level_launch(tsq_workspace *ws, const KernelSet &ks) {
   return L;
 }
 
-cudaError_t launch_level(const KernelSet &ks, const LevelLaunch &L, Params **dst,
+// (the partition and schedule kernels also take the control block's address
+// by value -- it never moves for a workspace -- so their first read of it does
+// not wait for the read of the parameter block)
+cudaError_t launch_level(const KernelSet &ks, const LevelLaunch &L, Params **dst, Ctl **ctl,
                          cudaStream_t s) {
-  void *args[1] = {dst};
+  void *args[2] = {dst, ctl};
   cudaError_t e = cudaLaunchKernel(ks.part, L.part_grid, dim3(kPartThreads), args, ks.part_smem, s);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernel(ks.sched, L.sched_grid, dim3(kThreads), args, ks.sched_smem, s);
@@ -411,7 +414,8 @@ tsq_status build_graph(tsq_workspace *ws, int kt, bool pay, GraphEntry *ge) {
   cudaGraph_t body = ip.conditional.phGraph_out[0];
 
   Params *dp = ws->d_params;
-  void *dev_args[1] = {&dp};
+  Ctl *dctl = ws->d_ctl;
+  void *dev_args[2] = {&dp, &dctl};
   const LevelLaunch LL = level_launch(ws, ks);
   cudaKernelNodeParams pk = cudaKernelNodeParams{};
   pk.func = const_cast<void *>(ks.part);
@@ -810,7 +814,7 @@ tsq_status tsq_sort(void *keys, void *payload, size_t n, tsq_dtype key_t, tsq_dt
   TSQ_CUDA(cudaEventRecord(t0, s));
   void *iargs[2] = {&pv, &dst};
   TSQ_CUDA(cudaLaunchKernel(ks.init, dim3(1), dim3(kThreads), iargs, 0, s));
-  void *largs[1] = {&dst};
+  void *largs[2] = {&dst, &ws->d_ctl};
   const LevelLaunch LL = level_launch(ws, ks);
   float total_levels = 0.f;
   ws->level_bytes.clear();
@@ -939,10 +943,10 @@ tsq_status tsq_partition_segment(const void *keys, const void *payload, void *ou
   Params *dst = ws->d_params;
   void *iargs[2] = {&pv, &dst};
   TSQ_CUDA(cudaLaunchKernel(ks.init, dim3(1), dim3(kThreads), iargs, 0, s));
-  void *largs[1] = {&dst};
+  void *largs[2] = {&dst, &ws->d_ctl};
   st = prepare_small_smem(ks);
   if (st != TSQ_OK) return st;
-  TSQ_CUDA(launch_level(ks, level_launch(ws, ks), &dst, s));
+  TSQ_CUDA(launch_level(ks, level_launch(ws, ks), &dst, &ws->d_ctl, s));
   TSQ_CUDA(cudaLaunchKernel(ks.retire, dim3(occupancy_grid(ws, ks.retire, 0)), dim3(kThreads),
                             largs, 0, s));
   if (staged) {

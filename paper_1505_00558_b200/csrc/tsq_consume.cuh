@@ -569,7 +569,8 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
 }
 
 template <class C, bool PAY>
-__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ Pg) {
+__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params *__restrict__ Pg,
+                                                                    Ctl *ctl) {
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   // every role reads the launch parameters per tile: keep a copy on chip
@@ -587,7 +588,11 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(const Params
   __shared__ StageCounts sc[G::STAGES];
   __shared__ CounterShare cshare[G::STAGES];
 
-  Ctl *ctl = Pg->ctl;  // (the on-chip copy is complete after the barrier below)
+  // (ctl by value: its read runs beside the copy of the parameter block,
+  // which is complete after the barrier below)
+#ifdef TSQ_EXP_CTL_FROM_PARAMS
+  ctl = Pg->ctl;
+#endif
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u);
   const uint32_t ntiles = ctl->cur_ntiles;

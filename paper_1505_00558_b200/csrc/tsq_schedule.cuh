@@ -715,13 +715,17 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
 }
 
 template <class C, bool PAY>
-__global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__restrict__ P) {
+__global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__restrict__ P,
+                                                            Ctl *ctl) {
   typedef typename C::U U;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ u64 st[ST_COUNT];
   __shared__ uint32_t bcast[2];
   __shared__ RoundShared rs;
-  Ctl *ctl = P->ctl;
+  // (ctl by value: this read does not wait for the parameter block's)
+#ifdef TSQ_EXP_CTL_FROM_PARAMS
+  ctl = P->ctl;
+#endif
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u), nxt = cur ^ 1;
   const uint32_t nseg = ctl->cur_nseg;
