@@ -55,6 +55,36 @@ struct StageCounts {
   u64 tot;                // the tile's (<, ==, >) totals, same packing
 };
 
+// One key against the pivot: two compares and two predicated increments.
+// (The compiler's code for `lt += x < piv` is an add plus a predicated move
+// per side in one serial chain per counter; a counter lane counts 48 keys of
+// a tile, and the counter warps' 1.7 us per tile -- per-tile timeline,
+// scripts/trace_level.py -- is the longest stage of a pass whose data comes
+// from L2.)  Callers keep one pair of counters per vector element, so the
+// dependent chains are a quarter as long.
+template <bool SIGNED>
+__device__ __forceinline__ void count_key(uint32_t &lt, uint32_t &gt, uint32_t x, uint32_t piv) {
+  if (SIGNED)
+    asm("{\n\t.reg .pred pl, pg;\n\tsetp.lt.s32 pl, %2, %3;\n\tsetp.gt.s32 pg, %2, %3;\n\t"
+        "@pl add.u32 %0, %0, 1;\n\t@pg add.u32 %1, %1, 1;\n\t}"
+        : "+r"(lt), "+r"(gt) : "r"(x), "r"(piv));
+  else
+    asm("{\n\t.reg .pred pl, pg;\n\tsetp.lt.u32 pl, %2, %3;\n\tsetp.gt.u32 pg, %2, %3;\n\t"
+        "@pl add.u32 %0, %0, 1;\n\t@pg add.u32 %1, %1, 1;\n\t}"
+        : "+r"(lt), "+r"(gt) : "r"(x), "r"(piv));
+}
+template <bool SIGNED>
+__device__ __forceinline__ void count_key(uint32_t &lt, uint32_t &gt, u64 x, u64 piv) {
+  if (SIGNED)
+    asm("{\n\t.reg .pred pl, pg;\n\tsetp.lt.s64 pl, %2, %3;\n\tsetp.gt.s64 pg, %2, %3;\n\t"
+        "@pl add.u32 %0, %0, 1;\n\t@pg add.u32 %1, %1, 1;\n\t}"
+        : "+r"(lt), "+r"(gt) : "l"(x), "l"(piv));
+  else
+    asm("{\n\t.reg .pred pl, pg;\n\tsetp.lt.u64 pl, %2, %3;\n\tsetp.gt.u64 pg, %2, %3;\n\t"
+        "@pl add.u32 %0, %0, 1;\n\t@pg add.u32 %1, %1, 1;\n\t}"
+        : "+r"(lt), "+r"(gt) : "l"(x), "l"(piv));
+}
+
 // one consumer warp's keys of a stage, counted by a counter lane in the
 // order the consumer will rank them; FULL: the whole tile is the segment's
 // RAWCMP: the stage holds the caller's encoding of a kRawOrder key type --
@@ -65,6 +95,27 @@ __device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, 
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   uint32_t lt = 0, gt = 0, va = 0;
+#ifndef TSQ_EXP_OLD_COUNT
+  if (FULL) {
+    uint32_t l4[G::VN], g4[G::VN];
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) l4[q] = g4[q] = 0;
+#pragma unroll
+    for (int v = 0; v < G::VPT; ++v) {
+      const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
+      U key[G::VN];
+      unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+#pragma unroll
+      for (int q = 0; q < G::VN; ++q) {
+        const U x = RAWCMP ? key[q] : (raw ? C::enc(key[q]) : key[q]);
+        count_key<RAWCMP && C::kSigned>(l4[q], g4[q], x, piv);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < G::VN; ++q) { lt += l4[q]; gt += g4[q]; }
+    return lt | (gt << 10) | ((uint32_t)G::IPT << 20);
+  }
+#endif
 #pragma unroll
   for (int v = 0; v < G::VPT; ++v) {
     const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
