@@ -95,8 +95,12 @@ __device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, 
   typedef typename C::U U;
   typedef Geo<C, PAY> G;
   uint32_t lt = 0, gt = 0, va = 0;
-#ifndef TSQ_EXP_OLD_COUNT
-  if (FULL) {
+#ifdef TSQ_EXP_OLD_COUNT
+  constexpr bool kLean = false;
+#else
+  constexpr bool kLean = FULL;
+#endif
+  if constexpr (kLean) {
     uint32_t l4[G::VN], g4[G::VN];
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) l4[q] = g4[q] = 0;
@@ -113,32 +117,32 @@ __device__ __forceinline__ uint32_t count_slice(const typename C::U *sk, int w, 
     }
 #pragma unroll
     for (int q = 0; q < G::VN; ++q) { lt += l4[q]; gt += g4[q]; }
-    return lt | (gt << 10) | ((uint32_t)G::IPT << 20);
-  }
-#endif
+    va = G::IPT;
+  } else {
 #pragma unroll
-  for (int v = 0; v < G::VPT; ++v) {
-    const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
-    U key[G::VN];
-    unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
+    for (int v = 0; v < G::VPT; ++v) {
+      const int e0 = (v * kConsumers + w * 32 + lane) * G::VN;
+      U key[G::VN];
+      unpack(*reinterpret_cast<const typename Vec<U>::K *>(sk + e0), key);
 #pragma unroll
-    for (int q = 0; q < G::VN; ++q) {
-      const U x = RAWCMP ? key[q] : (raw ? C::enc(key[q]) : key[q]);
-      const bool below = RAWCMP ? C::rlt(x, piv) : x < piv;
-      const bool above = RAWCMP ? C::rlt(piv, x) : x > piv;
-      if (FULL) {
-        lt += below ? 1u : 0u;
-        gt += above ? 1u : 0u;
-      } else {
-        const int idx = e0 + q;
-        const bool valid = idx >= rlo && idx < rhi;
-        lt += (valid && below) ? 1u : 0u;
-        gt += (valid && above) ? 1u : 0u;
-        va += valid ? 1u : 0u;
+      for (int q = 0; q < G::VN; ++q) {
+        const U x = RAWCMP ? key[q] : (raw ? C::enc(key[q]) : key[q]);
+        const bool below = RAWCMP ? C::rlt(x, piv) : x < piv;
+        const bool above = RAWCMP ? C::rlt(piv, x) : x > piv;
+        if (FULL) {
+          lt += below ? 1u : 0u;
+          gt += above ? 1u : 0u;
+        } else {
+          const int idx = e0 + q;
+          const bool valid = idx >= rlo && idx < rhi;
+          lt += (valid && below) ? 1u : 0u;
+          gt += (valid && above) ? 1u : 0u;
+          va += valid ? 1u : 0u;
+        }
       }
     }
+    if (FULL) va = G::IPT;
   }
-  if (FULL) va = G::IPT;
   return lt | (gt << 10) | (va << 20);
 }
 

@@ -59,6 +59,11 @@ struct Seg {
   long long begin, end;
   u64 pivot;
   u64 klo, khi;
+  // atomic placement: the (<, >) ranges its tiles have reserved so far, and
+  // after the pass the segment's totals -- read with the record by the
+  // scheduling (no further round trip); look-back placement keeps its
+  // descriptors in lookback[]
+  u64 fill;
   uint32_t tile_base, ntiles;
   uint32_t buf, kind, depth, noverify;
   uint32_t eq_fill;  // records, atomic placement: == payload slots reserved so far

@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
     u64 *z = reinterpret_cast<u64 *>(ctl);
     for (unsigned i = 0; i < sizeof(Ctl) / sizeof(u64); ++i) z[i] = 0ull;
   }
-  for (uint32_t i = threadIdx.x; i < pv.tile_cap; i += kThreads) pv.lookback[0][i] = 0ull;
+  if (pv.reproducible)
+    for (uint32_t i = threadIdx.x; i < pv.tile_cap; i += kThreads) pv.lookback[0][i] = 0ull;
   __syncthreads();
   const long long n = pv.n;
   const long long T = Geo<C, PAY>::TILE;
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) init_kernel(Params pv, Params *P) {
       s.klo = 0; s.khi = (u64)KeyMax<U>::v;  // the whole (encoded) key space
       s.tile_base = 0; s.ntiles = ntiles;
       s.buf = buf; s.kind = kind; s.depth = 1; s.noverify = 0; s.eq_fill = 0; s.fail = 0;
+      s.fill = 0;
       pv.segs[0][0] = s;
       ctl->cur_nseg = 1;
       ctl->cur_ntiles = ntiles;
@@ -216,7 +218,8 @@ __global__ void __launch_bounds__(kThreads) export_level_kernel(const Params *__
     rec.new_l = -1;
     rec.new_r = -1;
     if (sg.kind == KIND_PARTITION) {
-      const u64 inc = P->lookback[cur][sg.tile_base + (P->reproducible ? sg.ntiles - 1 : 0)];
+      const u64 inc =
+          P->reproducible ? P->lookback[cur][sg.tile_base + sg.ntiles - 1] : sg.fill;
       const long long lt = (long long)((inc >> 31) & 0x7fffffffull);
       const long long gt = (long long)(inc & 0x7fffffffull);
       const int db = (int)sg.buf ^ 1;

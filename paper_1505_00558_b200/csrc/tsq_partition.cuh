@@ -283,7 +283,8 @@ __device__ __forceinline__ void lookback_loop(const Params *P, int cur, u64 *agg
       // verified by the counters: nothing to place
     } else if (!reproducible) {
       if (lane == 0) {
-        const u64 ex = atomicAdd(reinterpret_cast<unsigned long long *>(&lb[m.tile_base]), m.agg);
+        const u64 ex = atomicAdd(
+            reinterpret_cast<unsigned long long *>(&P->segs[cur][m.sid].fill), m.agg);
         const uint32_t eqx = PAY ? atomicAdd(&P->segs[cur][m.sid].eq_fill, m.eq_excl) : 0u;
         m.excl = ex;
         m.eq_excl = eqx;

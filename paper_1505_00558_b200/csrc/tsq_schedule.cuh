@@ -309,8 +309,8 @@ __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u
     return false;
   }
   // the segment's (<, >) totals: the last tile's inclusive descriptor, or
-  // the fill word all its tiles reserved from
-  const u64 inc = P->lookback[cur][sg.tile_base + (P->reproducible ? sg.ntiles - 1 : 0)];
+  // the record's fill word all its tiles reserved from
+  const u64 inc = P->reproducible ? P->lookback[cur][sg.tile_base + sg.ntiles - 1] : sg.fill;
   const long long lt = (long long)((inc >> 31) & 0x7fffffffull);
   const long long gt = (long long)(inc & 0x7fffffffull);
   const long long eq = len - lt - gt;
@@ -550,7 +550,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
           s.klo = q.klo; s.khi = q.khi;
           s.tile_base = ltile; s.ntiles = q.ntiles;
           s.buf = q.buf; s.kind = q.kind; s.depth = q.depth; s.noverify = q.noverify;
-          s.eq_fill = 0; s.fail = 0;
+          s.eq_fill = 0; s.fail = 0; s.fill = 0;
           P->segs[nxt][lslot] = s;
         }
         uint32_t *tm = P->tilemap[nxt] + ltile;
@@ -601,7 +601,7 @@ __device__ void cta_append_level(const Params *P, int nxt, long long begin, long
       s.klo = klo; s.khi = khi;
       s.tile_base = tbase; s.ntiles = ntiles;
       s.buf = buf; s.kind = kind; s.depth = depth; s.noverify = noverify;
-      s.eq_fill = 0; s.fail = 0;
+      s.eq_fill = 0; s.fail = 0; s.fill = 0;
       P->segs[nxt][slot] = s;
     } else {
       atomicOr(&ctl->error, (uint32_t)ERR_CAPACITY);
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u), nxt = cur ^ 1;
   const uint32_t nseg = ctl->cur_nseg;
-  {
+  if (P->reproducible) {  // the next level's look-back descriptors
     u64 *lbn = P->lookback[nxt];
     const uint32_t cap = P->tile_cap;
     for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < cap; i += gridDim.x * kThreads)
