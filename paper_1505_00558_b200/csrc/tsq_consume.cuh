@@ -557,6 +557,22 @@ __device__ __forceinline__ void emit_tile(const Params *P, uint32_t it, typename
     if (ul) { plt = (uint32_t)o_lt + w_lt + lane; st_lt = 32; }
     if (ug) { pgt = (uint32_t)o_gt + t_gt - 1u - w_gt - lane; st_gt = 32; }
   }
+#ifdef TSQ_DEBUG_CHECKS
+  if (!PAY && full) {
+    // this thread's slots (first, step, count per side) lie inside the runs
+    uint32_t nl = 0, ng = 0;
+    const bool rr = src_raw && dst_raw && C::kRawOrder;
+    const U pq = rr ? C::dec(piv) : piv;
+#pragma unroll
+    for (int i = 0; i < G::IPT; ++i) {
+      const U x = rr ? key[i] : (src_raw ? C::enc(key[i]) : key[i]);
+      nl += (rr ? C::rlt(x, pq) : x < pq) ? 1u : 0u;
+      ng += (rr ? C::rlt(pq, x) : x > pq) ? 1u : 0u;
+    }
+    TSQ_CHECK(nl == 0 || (plt >= (uint32_t)o_lt && plt + (nl - 1) * st_lt < (uint32_t)o_lt + t_lt));
+    TSQ_CHECK(ng == 0 || (pgt < (uint32_t)o_gt + t_gt && pgt >= (uint32_t)o_gt + (ng - 1) * st_gt));
+  }
+#endif
   named_sync(1, kConsumers);  // every consumer holds its keys: restage in place
 #if defined(TSQ_EXP_COPY) && !defined(TSQ_EXP_STAGE)
   if (full) {  // experiment: pipeline ceiling -- the tile goes out unpartitioned
