@@ -17,9 +17,26 @@
 
 namespace tsq {
 
+// phase stamps of CTA 0 / warp 0 (profiling builds only: -DTSQ_SCHED_CLOCK;
+// printed at kernel end for level TSQ_SCHED_CLOCK)
+#ifdef TSQ_SCHED_CLOCK
+#include <cstdio>
+__device__ unsigned long long g_sc[16];
+#define TSQ_SC(i)                                                         \
+  do {                                                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                            \
+      unsigned long long t_;                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+      g_sc[i] = t_;                                                       \
+    }                                                                     \
+  } while (0)
+#else
+#define TSQ_SC(i) ((void)0)
+#endif
 
-
-// per-CTA statistics (shared-memory atomics, one global flush per CTA)
+// per-CTA statistics: one slice per warp, written by that warp's leader lane
+// alone (plain updates: 64-bit shared-memory atomics are compare-and-swap
+// loops, ~0.7 us of the segment head), summed into one global flush per CTA
 enum SchedStat {
   ST_STAGES, ST_SORTED, ST_REVERSED, ST_DEPTH, ST_BYTES_PART, ST_BYTES_RETIRE, ST_W0, ST_W1,
   ST_FALLBACK, ST_PARTITIONED, ST_EQ_RUNS, ST_EQ_ELEMS, ST_BISECTED, ST_COUNT
@@ -293,17 +310,17 @@ __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u
     if (sg.fail == 0) {
       const uint32_t rk = sg.kind == KIND_VERIFY_ASC ? RUN_SORTED : RUN_REVERSED;
       if (leader) {
-        atomicAdd(&st[ST_STAGES], 1ull);
-        atomicAdd(&st[rk == RUN_SORTED ? ST_SORTED : ST_REVERSED], 1ull);
-        atomicMax(&st[ST_DEPTH], (u64)sg.depth);
-        atomicAdd(&st[ST_BYTES_PART], (u64)len * kb);  // the verify read
+        st[ST_STAGES] += 1ull;
+        st[rk == RUN_SORTED ? ST_SORTED : ST_REVERSED] += 1ull;
+        st[ST_DEPTH] = st[ST_DEPTH] > (u64)sg.depth ? st[ST_DEPTH] : (u64)sg.depth;
+        st[ST_BYTES_PART] += (u64)len * kb;  // the verify read
         if (!(rk == RUN_SORTED && sg.buf == 0)) {
-          atomicAdd(&st[ST_BYTES_RETIRE], 2ull * (u64)len * (u64)(kb + (PAY ? 4 : 0)));
-          atomicAdd(&st[ST_W0], (u64)len);
+          st[ST_BYTES_RETIRE] += 2ull * (u64)len * (u64)(kb + (PAY ? 4 : 0));
+          st[ST_W0] += (u64)len;
         }
       }
     } else {
-      if (leader) atomicAdd(&st[ST_FALLBACK], 1ull);
+      if (leader) st[ST_FALLBACK] += 1ull;
       *requeue = 1;
     }
     return false;
@@ -318,19 +335,19 @@ __device__ bool segment_head(const Params *P, int nxt, const Seg &sg, int cur, u
   *gt_out = gt;
   if (!bookkeep) return !P->single_stage;
   if (leader) {
-    atomicAdd(&st[ST_STAGES], 1ull);
-    atomicAdd(&st[ST_PARTITIONED], (u64)len);
-    atomicMax(&st[ST_DEPTH], (u64)sg.depth);
+    st[ST_STAGES] += 1ull;
+    st[ST_PARTITIONED] += (u64)len;
+    st[ST_DEPTH] = st[ST_DEPTH] > (u64)sg.depth ? st[ST_DEPTH] : (u64)sg.depth;
     u64 bytes = (u64)len * kb + (u64)(lt + gt) * kb;
     if (PAY) bytes += (u64)len * 8ull;
-    atomicAdd(&st[ST_BYTES_PART], bytes);
-    atomicAdd(&st[sg.buf == 0 ? ST_W1 : ST_W0], (u64)(lt + gt));
-    if (PAY) atomicAdd(&st[ST_W1], (u64)eq);
+    st[ST_BYTES_PART] += bytes;
+    st[sg.buf == 0 ? ST_W1 : ST_W0] += (u64)(lt + gt);
+    if (PAY) st[ST_W1] += (u64)eq;
     if (eq > 0) {
-      atomicAdd(&st[ST_EQ_RUNS], 1ull);
-      atomicAdd(&st[ST_EQ_ELEMS], (u64)eq);
-      atomicAdd(&st[ST_BYTES_RETIRE], (u64)eq * (kb + (PAY ? 8 : 0)));
-      atomicAdd(&st[ST_W0], (u64)eq);
+      st[ST_EQ_RUNS] += 1ull;
+      st[ST_EQ_ELEMS] += (u64)eq;
+      st[ST_BYTES_RETIRE] += (u64)eq * (kb + (PAY ? 8 : 0));
+      st[ST_W0] += (u64)eq;
     }
     if (P->single_stage) {
       ctl->stage_lt = (u64)lt;
@@ -402,10 +419,15 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     const uint32_t sid = task >> 1;
     const int c = (int)(task & 1u);
     const Seg sg = P->segs[cur][sid];
+#ifdef TSQ_SCHED_CLOCK
+    if (sg.end < 0) return;  // (never: keeps the stamp behind the load)
+#endif
+    TSQ_SC(2);
     long long lt = 0, gt = 0;
     uint32_t requeue = 0;
     const bool kids =
         segment_head<C, PAY, false>(P, nxt, sg, cur, st, &lt, &gt, &requeue, c == 0);
+    TSQ_SC(3);
     const long long len = sg.end - sg.begin;
     if (lane == 0 && c == 0) {
       if (sg.kind != KIND_PARTITION) {
@@ -442,7 +464,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         if (lane == 0) {
           ReqSmall &q = rs.sm[warp][0];
           q.begin = cb; q.len = cl; q.buf = db; q.valid = 1;
-          atomicMax(&st[ST_DEPTH], (u64)depth);
+          st[ST_DEPTH] = st[ST_DEPTH] > (u64)depth ? st[ST_DEPTH] : (u64)depth;
         }
       } else {
         u64 klo, khi;
@@ -451,7 +473,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
         u64 piv;
         if ((int)depth > P->max_depth) {  // depth guard: bisect the key bound
           piv = bisect_pivot(klo, khi);
-          if (lane == 0) atomicAdd(&st[ST_BISECTED], 1ull);
+          if (lane == 0) st[ST_BISECTED] += 1ull;
         } else {
           // the samples are only loaded here; they are sorted after the
           // round's queue claims, whose round trip their loads overlap
@@ -474,7 +496,9 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
       }
     }
   }
+  TSQ_SC(4);
   __syncthreads();
+  TSQ_SC(5);
   // one claim per queue for the whole round, the queues' atomics issued by
   // separate lanes of warp 0 so their round trips overlap
   if (threadIdx.x < 2 + kSmallClasses) {
@@ -513,6 +537,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     }
   }
   __syncthreads();
+  TSQ_SC(6);
   if (S > 0) {
     // the pivot: median of the sorted samples; the order flag picks the
     // verification fast paths
@@ -527,6 +552,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     }
     __syncwarp();
   }
+  TSQ_SC(7);
   // each warp writes its records at its offsets
   uint32_t lslot = rs.lv_slot0, ltile = rs.lv_tile0, rslot = rs.run_slot0;
   uint32_t rchunk = rs.run_chunk0;
@@ -582,6 +608,7 @@ __device__ void schedule_round_warp(const Params *P, int cur, int nxt, uint32_t 
     for (uint32_t i = lane; i < q.nchunks; i += 32) cm[i] = rslot;
   }
   __syncthreads();  // the round's shared requests are consumed
+  TSQ_SC(8);
 }
 
 // CTA-wide appends (CTA mode: few segments, no contention to aggregate)
@@ -692,7 +719,7 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
     if (cl <= P->small_t) {
       if (threadIdx.x == 0) {
         append_small(P, cb, cl, db);
-        atomicMax(&st[ST_DEPTH], (u64)depth);
+        st[ST_DEPTH] = st[ST_DEPTH] > (u64)depth ? st[ST_DEPTH] : (u64)depth;
       }
       return;
     }
@@ -702,7 +729,7 @@ __device__ void schedule_segment_cta(const Params *P, int cur, int nxt, uint32_t
     u64 piv;
     if ((int)depth > P->max_depth) {  // depth guard: bisect the key bound
       piv = bisect_pivot(klo, khi);
-      if (threadIdx.x == 0) atomicAdd(&st[ST_BISECTED], 1ull);
+      if (threadIdx.x == 0) st[ST_BISECTED] += 1ull;
     } else {
       piv = (u64)cta_select_pivot_fast<C>(reinterpret_cast<const U *>(P->keys[db]), !P->raw[db],
                                           cb, cl, P->dran, P->mitigation, xk, bc, &flag);
@@ -719,24 +746,37 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
                                                             Ctl *ctl) {
   typedef typename C::U U;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ u64 st[ST_COUNT];
+  __shared__ u64 st_all[kThreads / 32][ST_COUNT];
   __shared__ uint32_t bcast[2];
   __shared__ RoundShared rs;
+  // the parameter block on chip (read all over the scheduling; its global
+  // copy costs a round trip at first touch), fetched beside the level state
+  __shared__ __align__(16) Params sparams;
+  static_assert(sizeof(Params) / 8 <= kThreads, "Params copy");
+  if (threadIdx.x < sizeof(Params) / 8)
+    reinterpret_cast<u64 *>(&sparams)[threadIdx.x] = reinterpret_cast<const u64 *>(P)[threadIdx.x];
+  P = &sparams;  // (complete after the barrier below)
+  u64 *st = st_all[threadIdx.x >> 5];
   // (ctl by value: this read does not wait for the parameter block's)
 #ifdef TSQ_EXP_CTL_FROM_PARAMS
   ctl = P->ctl;
 #endif
+  TSQ_SC(0);
   const uint32_t level = ctl->level;
   const int cur = (int)(level & 1u), nxt = cur ^ 1;
   const uint32_t nseg = ctl->cur_nseg;
+  for (int i = threadIdx.x; i < (kThreads / 32) * ST_COUNT; i += kThreads) (&st_all[0][0])[i] = 0ull;
+  __syncthreads();
   if (P->reproducible) {  // the next level's look-back descriptors
     u64 *lbn = P->lookback[nxt];
     const uint32_t cap = P->tile_cap;
     for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < cap; i += gridDim.x * kThreads)
       lbn[i] = 0ull;
   }
-  if (threadIdx.x < ST_COUNT) st[threadIdx.x] = 0ull;
-  __syncthreads();
+#ifdef TSQ_SCHED_CLOCK
+  if (level == 0xffffffffu) return;  // (never: keeps the stamp behind the read)
+#endif
+  TSQ_SC(1);
   const long long avg = nseg ? ((long long)ctl->cur_ntiles * Geo<C, PAY>::TILE) / nseg : 0;
   if (avg >= kCtaScheduleMin) {
     U *xk = reinterpret_cast<U *>(smem_raw);
@@ -751,14 +791,22 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
     }
   }
   __syncthreads();
-  if (threadIdx.x < ST_COUNT && st[threadIdx.x]) {
+  TSQ_SC(9);
+  u64 tot = 0;
+  if (threadIdx.x < ST_COUNT) {
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const u64 v = st_all[w][threadIdx.x];
+      tot = threadIdx.x == ST_DEPTH ? (tot > v ? tot : v) : tot + v;
+    }
+  }
+  if (threadIdx.x < ST_COUNT && tot) {
     u64 *dst[ST_COUNT] = {&ctl->stages, &ctl->sorted_bypass, &ctl->reversed_bypass,
                           &ctl->max_depth, &ctl->bytes_partition, &ctl->bytes_retire,
                           &ctl->writes0, &ctl->writes1, &ctl->verify_fallbacks,
                           &ctl->partitioned_elements, &ctl->eq_runs, &ctl->eq_elements,
                           &ctl->bisected};
-    if (threadIdx.x == ST_DEPTH) atomicMax(dst[ST_DEPTH], st[ST_DEPTH]);
-    else atomicAdd(dst[threadIdx.x], st[threadIdx.x]);
+    if (threadIdx.x == ST_DEPTH) atomicMax(dst[ST_DEPTH], tot);
+    else atomicAdd(dst[threadIdx.x], tot);
   }
   if (threadIdx.x == 0) {
     // one acquire-release counter bump per CTA (after the CTA barrier above
@@ -769,6 +817,7 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
                  : "=r"(d)
                  : "l"(&ctl->ctas_done)
                  : "memory");
+    TSQ_SC(10);
     if (d == gridDim.x - 1) {
       // the queue state the decision needs, read side by side with the
       // exchange of the append cursor
@@ -800,6 +849,17 @@ __global__ void __launch_bounds__(kThreads) schedule_kernel(const Params *__rest
       ctl->flush = flush ? 1u : 0u;
       // (the kernel boundary orders these writes before the next kernel)
       if (P->use_cond) cudaGraphSetConditional(P->cond, (more && !flush) ? 1u : 0u);
+#ifdef TSQ_SCHED_CLOCK
+      {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        if (level == TSQ_SCHED_CLOCK) {
+          printf("sched level %u nseg %u last-cta %u: ", level, nseg, blockIdx.x);
+          for (int i = 1; i <= 10; ++i) printf("%d:%lld ", i, (long long)(g_sc[i] - g_sc[0]));
+          printf("end:%lld ns\n", (long long)(t_ - g_sc[0]));
+        }
+      }
+#endif
     }
   }
 }
